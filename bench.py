@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Walk-engine benchmark (driver contract; BASELINE.json metric).
+
+Default workload = BASELINE.json configs[1]: Node2Vec (a=2, b=0.5, L=80),
+one query per vertex, synthetic R-MAT scale-22 edge-factor-16 graph, replay
+mode, seed 0.  A "step" is one pass of the walk kernel over all V queries.
+
+  value        sampled steps/s (sum of walk lengths / device time), inputs
+               resident in HBM, CUDA events on the launching stream, max over
+               ranks; graph + result pool (1.9 GB) exceed L2, so no flush.
+  e2e          the same metric through the C-ABI host-buffer call fw_walk
+               (H2D of the starts from pinned memory, D2H of sequences+lengths
+               into pinned memory inside the timed region).
+  roofline     algorithmic bytes per launch / mean launch time vs
+               the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  cpu_baseline the reference itself (baseline/_ref reswalk, numba, all host
+               threads) on a bounded sample of the same workload (rank 0, N=1).
+
+--impl reference times the reference's CPU implementation the same way
+(rank 0 only; other ranks exit 0).  Multi-GPU (torchrun): the graph is
+generated on rank 0 and broadcast over NCCL (off the timed path), each rank
+walks its own V queries with disjoint global qids (weak scaling, no
+collective on the walk path).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REASON_FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--scale", type=int, default=22)
+    p.add_argument("--app", default="node2vec",
+                   choices=["node2vec", "deepwalk", "ppr", "metapath"])
+    p.add_argument("--length", type=int, default=None)
+    p.add_argument("--queries", default="all", help="all | hub (PPR config)")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def app_config(args):
+    import paper_2404_08364_b200 as fw
+    if args.app == "node2vec":
+        return fw.AppConfig(app="node2vec", length=args.length or 80, a=2.0, b=0.5)
+    if args.app == "deepwalk":
+        return fw.AppConfig(app="deepwalk", length=args.length or 80)
+    if args.app == "ppr":
+        return fw.AppConfig(app="ppr", length=args.length or 80, stop_prob=0.2)
+    return fw.AppConfig(app="metapath", length=args.length or 5, schema=(0, 1, 2, 3, 4))
+
+
+def metric_name(args):
+    names = {"node2vec": "Node2Vec", "deepwalk": "DeepWalk", "ppr": "PPR", "metapath": "MetaPath"}
+    return f"{names[args.app]} sampled steps/sec"
+
+
+def workload_name(args, app):
+    extra = {"node2vec": " p=2 q=0.5", "ppr": " stop 0.2", "metapath": " schema 0..4",
+             "deepwalk": " weighted"}[args.app]
+    q = "all queries at the max-degree vertex" if args.queries == "hub" else "one query per vertex"
+    return f"{metric_name(args).split()[0]}{extra} length {app.length}, {q}, R-MAT scale-{args.scale} ef16"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             + ",".join(f"clocks_event_reasons.{r}" for r in REASON_FIELDS))
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        with open(self.path) as fh:
+            for line in fh:
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 5 + len(REASON_FIELDS):
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx.append(float(f[2]))
+                except ValueError:
+                    continue
+                for name, val in zip(REASON_FIELDS, f[5:]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def profiled_traffic(workload):
+    """dram bytes per launch of the walk kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as fh:
+            d = json.load(fh)
+        return d.get(workload)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (baseline/_ref reswalk) on a bounded sample
+# ---------------------------------------------------------------------------
+def import_reference():
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "nbc_ref"))
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "reswalk")) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    import reswalk  # noqa: F401
+    from reswalk import engine as E
+    from reswalk.apps import AppConfig
+    from reswalk.graph import Graph
+    return E, AppConfig, Graph
+
+
+def reference_runner(host_graph, app, starts_all):
+    """Returns (kind, run(n, offset) -> (sampled_steps, seconds), cores)."""
+    cores = os.cpu_count() or 1
+    try:
+        E, RAppConfig, RGraph = import_reference()
+        rg = RGraph(host_graph.vertex_count, host_graph.edge_count, host_graph.offsets,
+                    host_graph.targets, host_graph.weights, host_graph.labels)
+        rapp = RAppConfig(app=app.app, length=app.length, stop_prob=app.stop_prob, a=app.a,
+                          b=app.b, schema=tuple(app.schema), weighted=app.weighted)
+        eng = E.EngineConfig(workers=cores, replay=True)
+
+        def run(n, off):
+            total = [0]
+
+            def sink(b):
+                total[0] += int(b.lengths.astype(np.int64).sum())
+            t0 = time.perf_counter()
+            E.run(rg, starts_all[off:off + n], rapp, eng, seed=0, sink=sink)
+            return total[0], time.perf_counter() - t0
+        return "reference", run, cores
+    except ImportError:
+        import oracle
+
+        def run(n, off):
+            t0 = time.perf_counter()
+            _, ln, _ = oracle.walk(host_graph.offsets, host_graph.targets, host_graph.weights,
+                                   host_graph.labels, starts_all[off:off + n], app=app.app,
+                                   length=app.length, stop_prob=app.stop_prob, a=app.a,
+                                   b=app.b, schema=app.schema, base_qid=off, threads=cores)
+            return int(ln.astype(np.int64).sum()), time.perf_counter() - t0
+        return "port", run, cores
+
+
+def calibrate(run, seconds):
+    """Warm the JIT, then size a sample to ~`seconds` of CPU work."""
+    run(64, 0)
+    n = 256
+    while True:
+        s, t = run(n, 0)
+        if t > 1.0 or n >= 1 << 22:
+            break
+        n *= 4
+    rate_q = n / max(t, 1e-6)
+    return max(64, int(rate_q * seconds))
+
+
+def cpu_baseline(host_graph, app, starts_all, seconds):
+    kind, run, cores = reference_runner(host_graph, app, starts_all)
+    n = min(calibrate(run, seconds), len(starts_all))
+    sampled, t = run(n, 0)
+    return {"value": sampled / t, "unit": "steps/s", "cores": cores, "kind": kind,
+            "sample": f"{n} queries (global qids 0..{n - 1}) of the same workload, "
+                      f"{sampled} sampled steps in {t:.1f} s, replay mode, workers={cores}"}
+
+
+# ---------------------------------------------------------------------------
+def make_starts(args, nv, hub):
+    if args.queries == "hub":
+        return np.full(nv, hub, np.int64)
+    return np.arange(nv, dtype=np.int64)
+
+
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2404_08364_b200 import rmat
+    app = app_config(args)
+    g = rmat.rmat_graph(args.scale, labels=(args.app == "metapath"))
+    starts = make_starts(args, g.vertex_count, g.max_degree_vertex())
+    kind, run, cores = reference_runner(g, app, starts)
+    n = min(calibrate(run, min(args.cpu_seconds, 8.0)), len(starts))
+    for i in range(args.warmup):
+        run(n, (i * n) % max(1, len(starts) - n))
+    tot_s, tot_t = 0, 0.0
+    for i in range(args.steps):
+        s, t = run(n, ((args.warmup + i) * n) % max(1, len(starts) - n))
+        tot_s += s
+        tot_t += t
+    value = tot_s / tot_t
+    line = {
+        "impl": "reference", "metric": metric_name(args), "value": value, "unit": "steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * tot_t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp64+u64", "data": "synthetic",
+        "config": {"workload": workload_name(args, app), "graph": f"rmat-s{args.scale}-ef16",
+                   "sample_queries_per_step": n},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": kind,
+                         "sample": f"{n} queries per step, replay mode, workers={cores}"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_ours(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_08364_b200 as fw
+    from paper_2404_08364_b200 import _lib, rmat
+    from paper_2404_08364_b200.engine import DeviceGraph, _fw_structs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    app = app_config(args)
+    labels = args.app == "metapath"
+
+    # graph: generated on rank 0, replicated over NCCL (off the timed path)
+    if rank == 0:
+        dg = rmat.rmat_graph_device(args.scale, labels=labels, device=local)
+        arrs = [dg.offsets, dg.targets, dg.weights] + ([dg.labels] if labels else [])
+    V = 1 << args.scale
+    E_ = 16 * V
+    if world > 1:
+        if rank != 0:
+            arrs = [torch.empty(V + 1, dtype=torch.int64, device=dev),
+                    torch.empty(E_, dtype=torch.int32, device=dev),
+                    torch.empty(E_, dtype=torch.float32, device=dev)]
+            if labels:
+                arrs.append(torch.empty(E_, dtype=torch.uint8, device=dev))
+        for t in arrs:
+            dist.broadcast(t, src=0)
+        torch.cuda.synchronize()
+        if rank != 0:
+            dg = DeviceGraph(V, E_, *arrs[:3], arrs[3] if labels else None, device=local)
+    handle = dg.handle(local).ptr
+    hub = dg.max_degree_vertex()
+    n = V
+    base_qid = rank * n
+    starts_h = make_starts(args, n, hub)
+    starts = torch.from_numpy(starts_h).to(dev)
+    L = app.length
+    seq = torch.empty(n * L, dtype=torch.int32, device=dev)
+    lens = torch.empty(n, dtype=torch.int32, device=dev)
+    stats = torch.zeros(8, dtype=torch.int64, device=dev)
+    a_s, e_s, _schema = _fw_structs(app, fw.EngineConfig(replay=True))
+    stream = torch.cuda.current_stream(dev)
+
+    def launch():
+        _lib.check(lib.fw_walk_device(handle, starts.data_ptr(), n, base_qid, ctypes.byref(a_s),
+                                      ctypes.byref(e_s), 0, seq.data_ptr(), lens.data_ptr(),
+                                      stats.data_ptr(), stream.cuda_stream))
+
+    for _ in range(args.warmup):
+        launch()
+    torch.cuda.synchronize()
+    stats.zero_()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for i in range(args.steps):
+        launch()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    launch_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    my_ms = sum(launch_ms)
+    st = stats.cpu().numpy()
+    sampled = int(st[6])
+    alg_bytes = int(st[7])
+    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([sampled], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    elapsed_ms = float(t.item())
+    value = int(tot.item()) / (elapsed_ms / 1000.0)
+
+    # end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hs = torch.from_numpy(starts_h).pin_memory()
+        hseq = torch.empty(n * L, dtype=torch.int32).pin_memory()
+        hlen = torch.empty(n, dtype=torch.int32).pin_memory()
+        fst = _lib.FwStats()
+
+        def host_call():
+            _lib.check(lib.fw_walk(handle, hs.data_ptr(), n, base_qid, ctypes.byref(a_s),
+                                   ctypes.byref(e_s), 0, hseq.data_ptr(), hlen.data_ptr(),
+                                   ctypes.byref(fst)))
+        host_call()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_sampled = 0
+        for _ in range(args.steps):
+            host_call()
+            e2e_sampled += fst.sampled_steps
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        e2e_tot = torch.tensor([e2e_sampled], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+            dist.all_reduce(e2e_tot, op=dist.ReduceOp.SUM)
+        e2e = {"value": int(e2e_tot.item()) / float(e2e_s.item()), "unit": "steps/s",
+               "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * L * 4 + n * 4,
+               "path": "fw_walk (C ABI, pinned host buffers)"}
+        del hseq
+
+    peak, peak_kind = measured_peak()
+    mean_launch_s = (my_ms / args.steps) / 1000.0
+    achieved = (alg_bytes / args.steps) / mean_launch_s / 1e9
+    workload = workload_name(args, app)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_kind": peak_kind,
+                "traffic": profiled_traffic(workload),
+                "alg_bytes_per_launch": alg_bytes // args.steps,
+                "kernel": "fw::walk_kernel (persistent, 1 launch per step)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            host = dg.to_host()
+            cpu = cpu_baseline(host, app, starts_h, args.cpu_seconds)
+        except Exception as exc:  # report, never fail the GPU line
+            cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {type(exc).__name__}: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": metric_name(args), "value": value, "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp64+u64", "data": "synthetic",
+            "config": {"workload": workload, "graph": f"rmat-s{args.scale}-ef16",
+                       "vertices": V, "csr_entries": E_, "queries_per_gpu": n,
+                       "parallelism": f"replicated graph, qids partitioned x{world}",
+                       "l2": "inputs larger than L2 (graph + result pool > 126 MB), no flush",
+                       "sampled_steps_per_gpu_step": sampled // args.steps,
+                       "walk_attempts_per_step": int(st[0]) // args.steps},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

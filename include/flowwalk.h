@@ -1,0 +1,152 @@
+/*
+ * flowwalk.h -- C ABI of the B200-native walk engine (libflowwalk.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Every entry point returns
+ * an int status (FW_OK or one of the FW_E* codes) and records a message
+ * readable through fw_last_error().  The Python host layer
+ * (paper_2404_08364_b200/engine.py) maps the codes onto the reference's
+ * exception classes (reswalk errors.py:4-45).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   fw_graph_create / fw_graph_create_device / fw_graph_destroy
+ *       -- the read-only CSR arrays of reswalk.graph.Graph (pkg/src/reswalk/graph.py:40-87)
+ *          that the reference passes by reference into every step_pass call
+ *          (engine.py:209-221); here they are uploaded once and stay resident in HBM.
+ *   fw_walk / fw_walk_device
+ *       -- the worker loop Worker.run_batch / pass_once (engine.py:199-230) driving
+ *          the numba operator _kernels.step_pass (_kernels.py:320-483, 33 positional
+ *          args), for one batch of queries with global ids base_qid + i, plus the
+ *          sentinel pre-fill of the batch buffers (engine.py:299-300) and the
+ *          per-worker stats accumulation (engine.py:342-353).
+ *   fw_validate_device
+ *       -- _kernels.validate_walks (_kernels.py:486-546).
+ *   fw_rmat_edges_device / fw_synth_weights_device / fw_synth_labels_device
+ *       -- synthetic inputs; the reference only ships random/star edge lists and
+ *          numpy-seeded synthesis (graph.py:172-201, 257-277), see DESIGN.md.
+ */
+#ifndef FLOWWALK_H
+#define FLOWWALK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    FW_OK = 0,
+    FW_EVALIDATION = 1, /* reswalk ValidationError (engine.py:274-275, apps.py:48-59) */
+    FW_ECONFIG = 2,     /* reswalk ConfigError (engine.py:64-77, 276-277) */
+    FW_ECUDA = 3,       /* CUDA runtime failure */
+    FW_ENOMEM = 4,      /* device allocation failure */
+};
+
+/* app ids: reswalk apps.py:21-24 (APP_IDS) / _kernels.py:41-44 */
+enum { FW_APP_DEEPWALK = 0, FW_APP_PPR = 1, FW_APP_NODE2VEC = 2, FW_APP_METAPATH = 3 };
+/* sampler ids: _kernels.py:46-47 (resolved by EngineConfig.resolve_sampler, engine.py:79-87) */
+enum { FW_SAMPLER_ZPRS = 0, FW_SAMPLER_DPRS = 1 };
+/* fp64 summation order: auto picks tree-order scans when every partial sum
+ * is provably exact (so any order is bit-identical to the reference's
+ * sequential order), else the reference's sequential order. */
+enum { FW_ORDER_AUTO = 0, FW_ORDER_SEQUENTIAL = 1 };
+
+typedef struct fw_graph fw_graph;
+
+/* AppConfig (apps.py:38-59) as the step kernel consumes it (engine.py:213-215). */
+typedef struct {
+    int32_t app_id;
+    int32_t weighted;
+    uint32_t length;       /* l_max, < 2^20 */
+    uint32_t schema_len;   /* metapath only, else 0 */
+    const int64_t *schema; /* host pointer, schema_len entries */
+    double stop_prob;      /* ppr */
+    double inv_a;          /* 1.0 / a, computed by the caller in fp64 */
+    double inv_b;          /* 1.0 / b */
+} fw_app;
+
+/* EngineConfig (engine.py:51-87): only the bit-relevant fields. */
+typedef struct {
+    int32_t k_small;     /* 1 <= k_small <= k_big <= 1000 */
+    int32_t k_big;
+    int64_t d_t;         /* degree_threshold */
+    int32_t sampler_id;  /* FW_SAMPLER_* (already resolved) */
+    int32_t order_mode;  /* FW_ORDER_* */
+} fw_engine;
+
+/* RunStats counters (engine.py:245-260; _kernels.py:32-39) plus device metrics. */
+typedef struct {
+    int64_t steps;          /* ST_STEPS: attempts incl. terminal ones */
+    int64_t edges_scanned;  /* ST_EDGES */
+    int64_t collectives;    /* ST_COLLECTIVES */
+    int64_t draws;          /* ST_DRAWS */
+    int64_t small_tasks;    /* ST_SMALL */
+    int64_t large_tasks;    /* ST_LARGE */
+    int64_t sampled_steps;  /* sum of lengths */
+    int64_t alg_bytes;      /* algorithmic HBM bytes */
+    double kernel_ms;       /* walk kernel time (CUDA events) */
+    double total_ms;        /* incl. H2D/D2H for fw_walk */
+    int32_t exact_order;    /* 1 if tree-order scans were used */
+    int32_t grid_ctas;
+    int32_t kernel_launches;
+    int32_t reserved;
+} fw_stats;
+
+typedef struct {
+    int64_t max_degree;
+    int64_t max_degree_vertex;
+    float max_weight;
+    int32_t min_weight_lowbit_exp; /* min over w>0 of exponent of w's lowest set bit */
+    int32_t has_labels;
+    int32_t reserved;
+} fw_graph_info;
+
+const char *fw_last_error(void);
+int fw_device_count(int *out);
+
+/* Upload host CSR arrays once (pinned staging); labels may be NULL. */
+int fw_graph_create(const int64_t *offsets, const uint32_t *targets, const float *weights,
+                    const uint8_t *labels_or_null, uint64_t vertex_count, uint64_t edge_count,
+                    int device, fw_graph **out);
+/* Wrap device-resident CSR arrays already on `device` (borrowed, not freed). */
+int fw_graph_create_device(const int64_t *d_offsets, const uint32_t *d_targets,
+                           const float *d_weights, const uint8_t *d_labels_or_null,
+                           uint64_t vertex_count, uint64_t edge_count, int device,
+                           fw_graph **out);
+int fw_graph_destroy(fw_graph *g);
+int fw_graph_info_get(fw_graph *g, fw_graph_info *out);
+
+/* Host-buffer walk: H2D starts, walk, D2H sequences (n*length u32, sentinel
+ * padded) and lengths (n u32).  Stats are written (not accumulated). */
+int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t base_qid,
+            const fw_app *app, const fw_engine *eng, uint64_t seed,
+            uint32_t *out_seq, uint32_t *out_len, fw_stats *stats);
+
+/* Device-buffer walk, asynchronous on `stream` (a cudaStream_t, may be NULL).
+ * d_stats (int64[8], device) is ACCUMULATED: steps, edges, collectives, draws,
+ * small, large, sampled_steps, alg_bytes. */
+int fw_walk_device(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t base_qid,
+                   const fw_app *app, const fw_engine *eng, uint64_t seed,
+                   uint32_t *d_out_seq, uint32_t *d_out_len, int64_t *d_stats,
+                   void *stream);
+
+/* validate_walks on device; *d_bad (int64, device) accumulates violations. */
+int fw_validate_device(fw_graph *g, const int64_t *d_starts, uint64_t n,
+                       const uint32_t *d_seq, const uint32_t *d_len, uint32_t l_max,
+                       const int64_t *schema_host, uint32_t schema_len,
+                       int64_t *d_bad, void *stream);
+
+/* Synthetic R-MAT (Graph500 a,b,c; d = 1-a-b-c) edges, counter-hash driven so
+ * host (numpy) and device generate identical lists.  Writes m (src, dst)
+ * pairs for edge ids [e0, e0 + m). */
+int fw_rmat_edges_device(uint64_t seed, int32_t scale, double a, double b, double c,
+                         uint64_t e0, uint64_t m, uint32_t *d_src, uint32_t *d_dst,
+                         void *stream);
+/* w[e] = U[1,5) float32 from (seed, e); labels[e] = hash(seed, e) % label_count. */
+int fw_synth_weights_device(uint64_t seed, uint64_t e0, uint64_t m, float *d_w, void *stream);
+int fw_synth_labels_device(uint64_t seed, uint32_t label_count, uint64_t e0, uint64_t m,
+                           uint8_t *d_l, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

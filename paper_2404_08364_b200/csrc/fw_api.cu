@@ -1,0 +1,650 @@
+// C ABI of libflowwalk.so (declared in include/flowwalk.h): device-resident
+// CSR handle, walk launch (device and host buffers), GPU validator and the
+// synthetic-input generators.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/flowwalk.h"
+#include "fw_common.cuh"
+#include "fw_walk.cuh"
+
+using namespace fw;
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(expr)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return set_err(e_ == cudaErrorMemoryAllocation ? FW_ENOMEM : FW_ECUDA,       \
+                           "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__,    \
+                           __LINE__);                                                    \
+    } while (0)
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+constexpr int kQueueRing = 64;
+
+struct fw_graph {
+    int device = 0;
+    uint64_t V = 0, E = 0;
+    int64_t *off = nullptr;
+    uint32_t *tgt = nullptr;
+    float *w = nullptr;
+    uint8_t *lab = nullptr;
+    bool owned = false;
+    fw_graph_info info{};
+    unsigned long long *queues = nullptr;  // ring of per-launch cursors
+    unsigned call_counter = 0;
+    std::mutex mu;
+    std::mutex host_mu;  // serialises fw_walk's host-buffer scratch
+    // host-buffer walk scratch (grow-only)
+    DevBuf starts, seq, len, stats, schema;
+    std::vector<DevBuf> schema_ring;
+    int sm_count = 0;
+};
+
+extern "C" const char *fw_last_error(void) { return g_err.c_str(); }
+
+extern "C" int fw_device_count(int *out) {
+    CU(cudaGetDeviceCount(out));
+    return FW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Graph profile kernels (run once at upload).
+// ---------------------------------------------------------------------------
+__global__ void k_degree_max(const int64_t *__restrict__ off, uint64_t V,
+                             unsigned long long *out) {
+    unsigned long long best = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+        const unsigned long long key = (d << 32) | (0xFFFFFFFFull - (v & 0xFFFFFFFFull));
+        best = key > best ? key : best;
+    }
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long x = __shfl_xor_sync(FULL, best, o);
+        best = x > best ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+__global__ void k_weight_profile(const float *__restrict__ w, uint64_t E, int *minlow,
+                                 unsigned *maxbits, int *bad) {
+    int lo = INT_MAX;
+    unsigned mx = 0;
+    int b = 0;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const float x = w[e];
+        const unsigned bits = __float_as_uint(x);
+        if (!(x >= 0.0f) || isinf(x)) { b = 1; continue; }
+        if (x > 0.0f) {
+            const int ex = (bits >> 23) & 0xFF;
+            const unsigned man = bits & 0x7FFFFFu;
+            int low;
+            if (ex == 0) low = -149 + __ffs(man) - 1;
+            else low = ex - 150 + __ffs(man | 0x800000u) - 1;
+            lo = min(lo, low);
+            mx = max(mx, bits);
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+        mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+        b |= __shfl_xor_sync(FULL, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(minlow, lo);
+        atomicMax(maxbits, mx);
+        if (b) atomicOr(bad, 1);
+    }
+}
+
+static int profile_graph(fw_graph *g) {
+    unsigned long long *d_deg;
+    int *d_i;
+    CU(cudaMalloc(&d_deg, sizeof(unsigned long long)));
+    CU(cudaMalloc(&d_i, 3 * sizeof(int)));
+    CU(cudaMemset(d_deg, 0, sizeof(unsigned long long)));
+    int init[3] = {INT_MAX, 0, 0};
+    CU(cudaMemcpy(d_i, init, sizeof(init), cudaMemcpyHostToDevice));
+    const int grid = g->sm_count * 8;
+    if (g->V) k_degree_max<<<grid, 256>>>(g->off, g->V, d_deg);
+    if (g->E) k_weight_profile<<<grid, 256>>>(g->w, g->E, d_i, (unsigned *)(d_i + 1), d_i + 2);
+    CU(cudaGetLastError());
+    unsigned long long key = 0;
+    int res[3];
+    CU(cudaMemcpy(&key, d_deg, sizeof(key), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(res, d_i, sizeof(res), cudaMemcpyDeviceToHost));
+    cudaFree(d_deg);
+    cudaFree(d_i);
+    g->info.max_degree = g->V ? (int64_t)(key >> 32) : 0;
+    g->info.max_degree_vertex = g->V ? (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull)) : -1;
+    g->info.min_weight_lowbit_exp = res[0];
+    unsigned mb = (unsigned)res[1];
+    float mw;
+    memcpy(&mw, &mb, sizeof(mw));
+    g->info.max_weight = mw;
+    g->info.has_labels = g->lab != nullptr;
+    g->info.reserved = res[2];  // non-finite / negative weight flag
+    return FW_OK;
+}
+
+static int graph_common_init(fw_graph *g, int device) {
+    g->device = device;
+    CU(cudaSetDevice(device));
+    CU(cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaMalloc(&g->queues, kQueueRing * sizeof(unsigned long long)));
+    return FW_OK;
+}
+
+// Upload through a double-buffered pinned staging area.
+static int upload(void *dst, const void *src, size_t bytes, cudaStream_t st, void *pin[2],
+                  cudaEvent_t ev[2], size_t chunk) {
+    const char *s = (const char *)src;
+    char *d = (char *)dst;
+    int slot = 0;
+    for (size_t done = 0; done < bytes; done += chunk, slot ^= 1) {
+        const size_t n = std::min(chunk, bytes - done);
+        CU(cudaEventSynchronize(ev[slot]));
+        memcpy(pin[slot], s + done, n);
+        CU(cudaMemcpyAsync(d + done, pin[slot], n, cudaMemcpyHostToDevice, st));
+        CU(cudaEventRecord(ev[slot], st));
+    }
+    return FW_OK;
+}
+
+extern "C" int fw_graph_create(const int64_t *offsets, const uint32_t *targets,
+                               const float *weights, const uint8_t *labels, uint64_t V,
+                               uint64_t E, int device, fw_graph **out) {
+    if (!out || !offsets || (E && (!targets || !weights)))
+        return set_err(FW_EVALIDATION, "fw_graph_create: null array");
+    if (offsets[0] != 0 || (uint64_t)offsets[V] != E)
+        return set_err(FW_EVALIDATION, "offsets must start at 0 and end at edge_count");
+    fw_graph *g = new fw_graph();
+    int rc = graph_common_init(g, device);
+    if (rc) { delete g; return rc; }
+    g->V = V;
+    g->E = E;
+    g->owned = true;
+    auto fail = [&](int code) {
+        fw_graph_destroy(g);
+        return code;
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&g->off, (V + 1) * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&g->tgt, std::max<uint64_t>(E, 1) * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&g->w, std::max<uint64_t>(E, 1) * sizeof(float))) != cudaSuccess ||
+        (labels && (e = cudaMalloc(&g->lab, std::max<uint64_t>(E, 1))) != cudaSuccess))
+        return fail(set_err(FW_ENOMEM, "graph allocation: %s", cudaGetErrorString(e)));
+    const size_t chunk = 64u << 20;
+    void *pin[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2];
+    cudaStream_t st;
+    if (cudaMallocHost(&pin[0], chunk) != cudaSuccess || cudaMallocHost(&pin[1], chunk) != cudaSuccess)
+        return fail(set_err(FW_ENOMEM, "pinned staging allocation failed"));
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    cudaEventRecord(ev[0], st);
+    cudaEventRecord(ev[1], st);
+    rc = upload(g->off, offsets, (V + 1) * sizeof(int64_t), st, pin, ev, chunk);
+    if (!rc && E) rc = upload(g->tgt, targets, E * sizeof(uint32_t), st, pin, ev, chunk);
+    if (!rc && E) rc = upload(g->w, weights, E * sizeof(float), st, pin, ev, chunk);
+    if (!rc && E && labels) rc = upload(g->lab, labels, E, st, pin, ev, chunk);
+    cudaStreamSynchronize(st);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaStreamDestroy(st);
+    cudaFreeHost(pin[0]);
+    cudaFreeHost(pin[1]);
+    if (rc) return fail(rc);
+    if ((rc = profile_graph(g))) return fail(rc);
+    *out = g;
+    return FW_OK;
+}
+
+extern "C" int fw_graph_create_device(const int64_t *d_off, const uint32_t *d_tgt,
+                                      const float *d_w, const uint8_t *d_lab, uint64_t V,
+                                      uint64_t E, int device, fw_graph **out) {
+    if (!out || !d_off) return set_err(FW_EVALIDATION, "fw_graph_create_device: null array");
+    fw_graph *g = new fw_graph();
+    int rc = graph_common_init(g, device);
+    if (rc) { delete g; return rc; }
+    g->V = V;
+    g->E = E;
+    g->off = const_cast<int64_t *>(d_off);
+    g->tgt = const_cast<uint32_t *>(d_tgt);
+    g->w = const_cast<float *>(d_w);
+    g->lab = const_cast<uint8_t *>(d_lab);
+    g->owned = false;
+    if ((rc = profile_graph(g))) {
+        fw_graph_destroy(g);
+        return rc;
+    }
+    *out = g;
+    return FW_OK;
+}
+
+extern "C" int fw_graph_destroy(fw_graph *g) {
+    if (!g) return FW_OK;
+    cudaSetDevice(g->device);
+    if (g->owned) {
+        cudaFree(g->off);
+        cudaFree(g->tgt);
+        cudaFree(g->w);
+        if (g->lab) cudaFree(g->lab);
+    }
+    if (g->queues) cudaFree(g->queues);
+    g->starts.release();
+    g->seq.release();
+    g->len.release();
+    g->stats.release();
+    g->schema.release();
+    for (auto &b : g->schema_ring) b.release();
+    delete g;
+    return FW_OK;
+}
+
+extern "C" int fw_graph_info_get(fw_graph *g, fw_graph_info *out) {
+    if (!g || !out) return set_err(FW_EVALIDATION, "null handle");
+    *out = g->info;
+    return FW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Exact-order predicate: every app weight is an integer multiple
+// of 2^G and every per-step partial sum is <= d_max * x_max <= 2^(52+G), so
+// all fp64 partial sums are exact and any summation order reproduces the
+// reference's sequential `run += w` bit-for-bit.
+// ---------------------------------------------------------------------------
+static bool exact_order_ok(const fw_graph_info &gi, const fw_app &app) {
+    if (gi.reserved) return false;  // non-finite or negative weights: be literal
+    std::vector<double> F{1.0};
+    if (app.app_id == FW_APP_NODE2VEC) {
+        F.push_back(app.inv_a);
+        F.push_back(app.inv_b);
+    }
+    const bool weighted = app.weighted != 0;
+    if (weighted && !(gi.max_weight > 0.0f)) return true;  // every weight is zero
+    long G = LONG_MAX;
+    double xmax = 0.0;
+    for (double f : F) {
+        if (!(f > 0.0) || !std::isfinite(f)) return false;
+        int ex;
+        const double m = std::frexp(f, &ex);  // f = m * 2^ex, m in [0.5, 1)
+        uint64_t M = (uint64_t)std::ldexp(m, 53);
+        const int tz = __builtin_ctzll(M);
+        M >>= tz;
+        const int bits = 64 - __builtin_clzll(M);
+        const long low = (long)ex - 53 + tz;  // f = M * 2^low, M odd
+        if (weighted) {
+            if (bits + 24 > 53) return false;  // f * w would round
+            G = std::min(G, low + (long)gi.min_weight_lowbit_exp);
+            xmax = std::max(xmax, f * (double)gi.max_weight);
+        } else {
+            G = std::min(G, low);
+            xmax = std::max(xmax, f);
+        }
+    }
+    if (G < -1000) return false;
+    const double lim = std::ldexp(1.0, (int)(52 + G));
+    return (double)gi.max_degree * xmax <= lim;
+}
+
+static int check_cfg(fw_graph *g, const fw_app *app, const fw_engine *eng) {
+    if (!g || !app || !eng) return set_err(FW_EVALIDATION, "null argument");
+    if (app->app_id < 0 || app->app_id > 3) return set_err(FW_EVALIDATION, "unknown app id");
+    if (app->length < 1) return set_err(FW_EVALIDATION, "walk length must be >= 1");
+    if (app->length >= (1u << 20))
+        return set_err(FW_ECONFIG, "walk length exceeds the replay stream-id field");
+    if (app->app_id == FW_APP_METAPATH && app->schema_len == 0)
+        return set_err(FW_EVALIDATION, "metapath needs a non-empty schema");
+    if (!(1 <= eng->k_small && eng->k_small <= eng->k_big))
+        return set_err(FW_ECONFIG, "lane widths must satisfy 1 <= k_small <= k_big");
+    if (eng->k_big > 1000) return set_err(FW_ECONFIG, "k_big larger than the stream-id lane field");
+    if (eng->d_t < 1) return set_err(FW_ECONFIG, "degree threshold must be >= 1");
+    if (eng->sampler_id != FW_SAMPLER_ZPRS && eng->sampler_id != FW_SAMPLER_DPRS)
+        return set_err(FW_ECONFIG, "unknown sampler id");
+    return FW_OK;
+}
+
+static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t base_qid,
+                  const fw_app *app, const fw_engine *eng, uint64_t seed, uint32_t *d_seq,
+                  uint32_t *d_len, int64_t *d_stats, cudaStream_t stream, bool *exact_out,
+                  int *grid_out) {
+    if (base_qid + n > (1ull << 33))
+        return set_err(FW_ECONFIG, "query ids exceed the replay stream-id field (2^33)");
+    const bool exact = eng->order_mode == FW_ORDER_AUTO && exact_order_ok(g->info, *app);
+    if (exact_out) *exact_out = exact;
+    if (n == 0) return FW_OK;
+    WalkArgs a{};
+    a.off = g->off;
+    a.tgt = g->tgt;
+    a.w = g->w;
+    a.lab = g->lab;
+    a.starts = d_starts;
+    a.n = n;
+    a.base_qid = base_qid;
+    a.out_seq = d_seq;
+    a.out_len = d_len;
+    a.L = app->length;
+    a.weighted = app->weighted;
+    a.stop_prob = app->stop_prob;
+    a.inv_a = app->inv_a;
+    a.inv_b = app->inv_b;
+    a.k_small = eng->k_small;
+    a.k_big = eng->k_big;
+    a.d_t = eng->d_t;
+    a.h = mix64(seed + GOLDEN);
+    a.stats = (long long *)d_stats;
+    unsigned slot;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        slot = g->call_counter++ % kQueueRing;
+        if (g->schema_ring.empty()) g->schema_ring.resize(kQueueRing);
+    }
+    a.queue = g->queues + slot;
+    CU(cudaMemsetAsync(a.queue, 0, sizeof(unsigned long long), stream));
+    if (app->app_id == FW_APP_METAPATH) {
+        DevBuf &sb = g->schema_ring[slot];
+        CU(sb.reserve(app->schema_len * sizeof(int64_t)));
+        CU(cudaMemcpyAsync(sb.p, app->schema, app->schema_len * sizeof(int64_t),
+                           cudaMemcpyHostToDevice, stream));
+        a.schema = (const int64_t *)sb.p;
+        a.schema_len = app->schema_len;
+    }
+    const int occ = std::max(1, walk_occupancy(app->app_id, eng->sampler_id, exact));
+    const uint64_t warps_needed = n;
+    uint64_t grid = (uint64_t)g->sm_count * occ;
+    const uint64_t max_useful = (warps_needed + (kWalkThreads / 32) - 1) / (kWalkThreads / 32);
+    if (grid > max_useful) grid = max_useful;
+    if (grid_out) *grid_out = (int)grid;
+    CU(launch_walk(a, app->app_id, eng->sampler_id, exact, (int)grid, stream));
+    return FW_OK;
+}
+
+extern "C" int fw_walk_device(fw_graph *g, const int64_t *d_starts, uint64_t n,
+                              uint64_t base_qid, const fw_app *app, const fw_engine *eng,
+                              uint64_t seed, uint32_t *d_seq, uint32_t *d_len,
+                              int64_t *d_stats, void *stream) {
+    int rc = check_cfg(g, app, eng);
+    if (rc) return rc;
+    CU(cudaSetDevice(g->device));
+    return launch(g, d_starts, n, base_qid, app, eng, seed, d_seq, d_len, d_stats,
+                  (cudaStream_t)stream, nullptr, nullptr);
+}
+
+extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t base_qid,
+                       const fw_app *app, const fw_engine *eng, uint64_t seed,
+                       uint32_t *out_seq, uint32_t *out_len, fw_stats *stats) {
+    int rc = check_cfg(g, app, eng);
+    if (rc) return rc;
+    CU(cudaSetDevice(g->device));
+    std::lock_guard<std::mutex> lk(g->host_mu);
+    const uint64_t L = app->length;
+    CU(g->starts.reserve(std::max<uint64_t>(n, 1) * sizeof(int64_t)));
+    CU(g->seq.reserve(std::max<uint64_t>(n * L, 1) * sizeof(uint32_t)));
+    CU(g->len.reserve(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+    CU(g->stats.reserve(ST_COUNT * sizeof(int64_t)));
+    cudaStream_t st;
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1, e2, e3;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    cudaEventCreate(&e3);
+    cudaEventRecord(e0, st);
+    cudaMemsetAsync(g->stats.p, 0, ST_COUNT * sizeof(int64_t), st);
+    if (n) cudaMemcpyAsync(g->starts.p, starts, n * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    cudaEventRecord(e1, st);
+    bool exact = false;
+    int grid = 0;
+    rc = launch(g, (const int64_t *)g->starts.p, n, base_qid, app, eng, seed,
+                (uint32_t *)g->seq.p, (uint32_t *)g->len.p, (int64_t *)g->stats.p, st, &exact,
+                &grid);
+    cudaEventRecord(e2, st);
+    int64_t hst[ST_COUNT] = {0};
+    if (!rc) {
+        if (n) {
+            cudaMemcpyAsync(out_seq, g->seq.p, n * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(out_len, g->len.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+        }
+        cudaMemcpyAsync(hst, g->stats.p, sizeof(hst), cudaMemcpyDeviceToHost, st);
+        cudaEventRecord(e3, st);
+        cudaError_t ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess)
+            rc = set_err(FW_ECUDA, "walk failed: %s", cudaGetErrorString(ce));
+    }
+    if (!rc && stats) {
+        float kms = 0.f, tms = 0.f;
+        cudaEventElapsedTime(&kms, e1, e2);
+        cudaEventElapsedTime(&tms, e0, e3);
+        stats->steps = hst[ST_STEPS];
+        stats->edges_scanned = hst[ST_EDGES];
+        stats->collectives = hst[ST_COLLECTIVES];
+        stats->draws = hst[ST_DRAWS];
+        stats->small_tasks = hst[ST_SMALL];
+        stats->large_tasks = hst[ST_LARGE];
+        stats->sampled_steps = hst[ST_SAMPLED];
+        stats->alg_bytes = hst[ST_BYTES];
+        stats->kernel_ms = kms;
+        stats->total_ms = tms;
+        stats->exact_order = exact;
+        stats->grid_ctas = grid;
+        stats->kernel_launches = n ? 1 : 0;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
+// validate_walks on device (_kernels.py:486-546): one thread per query.
+// ---------------------------------------------------------------------------
+__global__ void k_validate(const int64_t *__restrict__ off, const uint32_t *__restrict__ tgt,
+                           const uint8_t *__restrict__ lab, const int64_t *__restrict__ starts,
+                           uint64_t n, const uint32_t *__restrict__ seq,
+                           const uint32_t *__restrict__ len, uint32_t L,
+                           const int64_t *__restrict__ schema, uint32_t schema_len,
+                           unsigned long long *bad) {
+    unsigned long long nb = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t cur = starts[i];
+        const int64_t ln = len[i];
+        if (ln > (int64_t)L) { nb++; continue; }
+        const uint32_t *row = seq + i * (uint64_t)L;
+        for (int64_t j = 0; j < ln; j++) {
+            const int64_t nxt = row[j];
+            int64_t lo = off[cur], hi = off[cur + 1], found = -1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                const int64_t tv = tgt[mid];
+                if (tv < nxt) lo = mid + 1;
+                else if (tv > nxt) hi = mid;
+                else { found = mid; break; }
+            }
+            if (found < 0) { nb++; break; }
+            if (schema_len > 0) {
+                if (j >= (int64_t)schema_len) { nb++; break; }
+                const int64_t want = schema[j];
+                bool ok = false;
+                for (int64_t e = found; e >= off[cur] && (int64_t)tgt[e] == nxt; e--)
+                    if ((lab ? (int64_t)lab[e] : 0) == want) { ok = true; break; }
+                for (int64_t e = found + 1; !ok && e < off[cur + 1] && (int64_t)tgt[e] == nxt; e++)
+                    if ((lab ? (int64_t)lab[e] : 0) == want) { ok = true; break; }
+                if (!ok) { nb++; break; }
+            }
+            cur = nxt;
+        }
+        for (int64_t j = ln; j < (int64_t)L; j++)
+            if (row[j] != 0xFFFFFFFFu) { nb++; break; }
+    }
+    if (nb) atomicAdd(bad, nb);
+}
+
+extern "C" int fw_validate_device(fw_graph *g, const int64_t *d_starts, uint64_t n,
+                                  const uint32_t *d_seq, const uint32_t *d_len, uint32_t L,
+                                  const int64_t *schema, uint32_t schema_len, int64_t *d_bad,
+                                  void *stream) {
+    if (!g) return set_err(FW_EVALIDATION, "null handle");
+    CU(cudaSetDevice(g->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t *d_schema = nullptr;
+    if (schema_len) {
+        CU(cudaMallocAsync(&d_schema, schema_len * sizeof(int64_t), st));
+        CU(cudaMemcpyAsync(d_schema, schema, schema_len * sizeof(int64_t),
+                           cudaMemcpyHostToDevice, st));
+    }
+    if (n)
+        k_validate<<<g->sm_count * 8, 128, 0, st>>>(g->off, g->tgt, g->lab, d_starts, n, d_seq,
+                                                   d_len, L, d_schema, schema_len,
+                                                   (unsigned long long *)d_bad);
+    CU(cudaGetLastError());
+    if (d_schema) CU(cudaFreeAsync(d_schema, st));
+    return FW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic inputs (counter-hash; paper_2404_08364_b200/rmat.py is the
+// bit-identical numpy twin).
+// ---------------------------------------------------------------------------
+__host__ __device__ static inline uint64_t perm_bits(uint64_t x, int s, uint64_t key) {
+    if (s == 0) return 0;
+    const uint64_t mask = s >= 64 ? ~0ull : ((1ull << s) - 1);
+    const int sh = (s + 1) / 2;
+    x = (x ^ key) & mask;
+    x = (x * GOLDEN) & mask;
+    x ^= x >> sh;
+    x = (x * MIX1) & mask;
+    x ^= x >> sh;
+    x = (x * MIX2) & mask;
+    x ^= x >> sh;
+    return x;
+}
+
+__global__ void k_rmat(uint64_t h, int s, uint32_t ta, uint32_t tab, uint32_t tabc,
+                       uint64_t pkey, uint64_t e0, uint64_t m, uint32_t *src, uint32_t *dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t base = mix64(h ^ ((e0 + i) * MIX1));
+        uint64_t u = 0, v = 0;
+        for (int l = 0; l < s; l++) {
+            const uint32_t r = (uint32_t)(mix64(base + (uint64_t)l * GOLDEN) >> 32);
+            const uint64_t sb = r >= tab;
+            const uint64_t db = (r >= ta && r < tab) || r >= tabc;
+            u = (u << 1) | sb;
+            v = (v << 1) | db;
+        }
+        src[i] = (uint32_t)perm_bits(u, s, pkey);
+        dst[i] = (uint32_t)perm_bits(v, s, pkey);
+    }
+}
+
+static uint32_t thresh(double p) {
+    if (p <= 0) return 0;
+    const double t = std::floor(p * 4294967296.0);
+    return t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t;
+}
+
+extern "C" int fw_rmat_edges_device(uint64_t seed, int32_t scale, double a, double b, double c,
+                                    uint64_t e0, uint64_t m, uint32_t *d_src, uint32_t *d_dst,
+                                    void *stream) {
+    if (scale < 0 || scale > 32) return set_err(FW_ECONFIG, "scale must be in [0, 32]");
+    if (a < 0 || b < 0 || c < 0 || a + b + c > 1.0)
+        return set_err(FW_ECONFIG, "R-MAT probabilities must be >= 0 and sum <= 1");
+    const uint64_t h = mix64(seed + GOLDEN);
+    const uint64_t pkey = mix64(seed ^ 0x5555555555555555ull);
+    if (m) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        k_rmat<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(h, scale, thresh(a), thresh(a + b),
+                                                         thresh(a + b + c), pkey, e0, m,
+                                                         d_src, d_dst);
+        CU(cudaGetLastError());
+    }
+    return FW_OK;
+}
+
+__global__ void k_synth_w(uint64_t h, uint64_t e0, uint64_t m, float *w) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = mix64(h + (e0 + i) * GOLDEN);
+        const double u = __dmul_rn(__ull2double_rn(z >> 11), 0x1.0p-53);
+        float x = __double2float_rn(__dadd_rn(1.0, __dmul_rn(4.0, u)));
+        if (x >= 5.0f) x = 4.99999952316284180f;  // nextafter(5, 1), graph.py:181-182
+        w[i] = x;
+    }
+}
+
+__global__ void k_synth_l(uint64_t h, uint32_t nl, uint64_t e0, uint64_t m, uint8_t *l) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = mix64(h + (e0 + i) * GOLDEN);
+        l[i] = (uint8_t)((z >> 32) % nl);
+    }
+}
+
+extern "C" int fw_synth_weights_device(uint64_t seed, uint64_t e0, uint64_t m, float *d_w,
+                                       void *stream) {
+    if (m) {
+        k_synth_w<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mix64(seed + GOLDEN), e0, m, d_w);
+        CU(cudaGetLastError());
+    }
+    return FW_OK;
+}
+
+extern "C" int fw_synth_labels_device(uint64_t seed, uint32_t label_count, uint64_t e0,
+                                      uint64_t m, uint8_t *d_l, void *stream) {
+    if (label_count < 1 || label_count > 256)
+        return set_err(FW_EVALIDATION, "label_count must be in [1, 256]");
+    if (m) {
+        k_synth_l<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mix64(seed + GOLDEN), label_count,
+                                                             e0, m, d_l);
+        CU(cudaGetLastError());
+    }
+    return FW_OK;
+}

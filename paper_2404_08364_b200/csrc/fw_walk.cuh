@@ -1,0 +1,35 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace fw {
+
+constexpr int kWalkThreads = 256;  // 8 warp walkers per CTA
+
+// Kernel arguments (passed by value through the constant bank).
+struct WalkArgs {
+    const int64_t *off;   // offsets int64[V+1]      (graph.py:44)
+    const uint32_t *tgt;  // targets uint32[E]       (graph.py:45)
+    const float *w;       // weights float32[E]      (graph.py:46)
+    const uint8_t *lab;   // labels uint8[E] or null (graph.py:47, 68-76)
+    const int64_t *starts;
+    uint64_t n;
+    uint64_t base_qid;
+    uint32_t *out_seq;    // n * L, sentinel padded
+    uint32_t *out_len;    // n
+    uint32_t L;
+    uint32_t schema_len;
+    const int64_t *schema;  // device copy
+    int32_t weighted;
+    double stop_prob, inv_a, inv_b;
+    int64_t k_small, k_big, d_t;
+    uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
+    unsigned long long *queue;
+    long long *stats;  // ST_COUNT counters (accumulated)
+};
+
+cudaError_t launch_walk(const WalkArgs &a, int app, int sampler, bool exact, int grid,
+                        cudaStream_t stream);
+int walk_occupancy(int app, int sampler, bool exact);
+
+}  // namespace fw

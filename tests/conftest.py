@@ -1,0 +1,58 @@
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+class Golden:
+    """Reference-generated walk vectors (tests/golden/gen_golden.py)."""
+
+    def __init__(self):
+        with open(os.path.join(GOLDEN, "cases.json")) as fh:
+            meta = json.load(fh)
+        self.cases = {c["name"]: c for c in meta["cases"]}
+        self.kats = meta["kats"]
+        self.z = np.load(os.path.join(GOLDEN, "walks.npz"))
+
+    def graph(self, name):
+        z = self.z
+        lab = z.get(f"g_{name}_labels")
+        return (z[f"g_{name}_offsets"], z[f"g_{name}_targets"], z[f"g_{name}_weights"], lab)
+
+    def expected(self, name):
+        z = self.z
+        return (z[f"c_{name}_seq"], z[f"c_{name}_len"], z[f"c_{name}_stats"])
+
+    def starts(self, name):
+        return self.z[f"c_{name}_starts"]
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return Golden()
+
+
+def case_kwargs(case):
+    """Flatten a golden case into oracle.walk keyword arguments."""
+    kw = dict(case["app"])
+    if "schema" in kw:
+        kw["schema"] = tuple(kw["schema"])
+    eng = dict(case["eng"])
+    for k in ("k_small", "k_big", "degree_threshold", "sampler"):
+        if k in eng:
+            kw[k] = eng[k]
+    kw["seed"] = case["seed"]
+    return kw, eng

@@ -1,0 +1,180 @@
+"""Parity of the sm_100a walk kernel (through the public API and the C ABI)
+against the reference's golden vectors and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import case_kwargs
+import paper_2404_08364_b200 as fw
+from paper_2404_08364_b200 import rmat
+
+pytestmark = pytest.mark.gpu
+
+STAT_NAMES = ("steps", "edges_scanned", "collectives", "draws", "small_tasks", "large_tasks")
+
+
+def _graph(golden, gname):
+    off, tgt, w, lab = golden.graph(gname)
+    return fw.Graph(len(off) - 1, len(tgt), off, tgt, w, lab)
+
+
+def _run(g, starts, app_cfg, eng_cfg, seed):
+    seqs, lens = [], []
+
+    def sink(b):
+        seqs.append(b.sequences.copy())
+        lens.append(b.lengths.copy())
+
+    st = fw.run(g, starts, app_cfg, eng_cfg, seed=seed, sink=sink)
+    return np.concatenate(seqs), np.concatenate(lens), st
+
+
+def _cases():
+    from conftest import Golden
+    return sorted(Golden().cases)
+
+
+@pytest.mark.parametrize("order", ["auto", "sequential"])
+@pytest.mark.parametrize("name", _cases())
+def test_golden_bit_exact(golden, name, order):
+    case = golden.cases[name]
+    g = _graph(golden, case["graph"])
+    app = dict(case["app"])
+    if "schema" in app:
+        app["schema"] = tuple(app["schema"])
+    eng = fw.EngineConfig(replay=True, order=order, **case["eng"])
+    seq, ln, st = _run(g, golden.starts(name), fw.AppConfig(**app), eng, case["seed"])
+    want_seq, want_len, want_stats = golden.expected(name)
+    np.testing.assert_array_equal(ln, want_len)
+    np.testing.assert_array_equal(seq, want_seq)
+    assert [getattr(st, f) for f in STAT_NAMES] == want_stats.tolist()
+    assert st.sampled_steps == int(want_len.sum())
+
+
+@pytest.fixture(scope="module")
+def s16():
+    return rmat.rmat_graph(16)
+
+
+@pytest.mark.parametrize("app", [
+    dict(app="deepwalk", length=80),
+    dict(app="node2vec", length=80, a=2.0, b=0.5),
+    dict(app="ppr", length=80, stop_prob=0.2),
+    dict(app="metapath", length=5, schema=(0, 1, 2, 3, 4)),
+])
+def test_rmat_s16_matches_oracle(s16, app):
+    """BASELINE config 1 shape (R-MAT s16 ef16, every vertex a query)."""
+    g = s16
+    starts = np.arange(g.vertex_count, dtype=np.int64)
+    if app["app"] == "ppr":
+        starts = np.full(20000, g.max_degree_vertex(), np.int64)
+    seq, ln, st = _run(g, starts, fw.AppConfig(**app), fw.EngineConfig(replay=True), 0)
+    kw = dict(app)
+    oseq, oln, ost = oracle.walk(g.offsets, g.targets, g.weights, g.labels, starts, **kw)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq, oseq)
+    assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()
+    assert st.exact_order
+    sch = app.get("schema", ()) if app["app"] == "metapath" else ()
+    assert oracle.validate(g.offsets, g.targets, g.labels, starts, seq, ln, sch) == 0
+
+
+def test_device_rmat_equals_host():
+    import torch
+    h = rmat.rmat_graph(14)
+    d = rmat.rmat_graph_device(14)
+    np.testing.assert_array_equal(d.offsets.cpu().numpy(), h.offsets)
+    np.testing.assert_array_equal(d.targets.cpu().numpy().view(np.uint32), h.targets)
+    np.testing.assert_array_equal(d.weights.cpu().numpy(), h.weights)
+    np.testing.assert_array_equal(d.labels.cpu().numpy(), h.labels)
+    assert d.max_degree() == h.max_degree()
+    assert d.max_degree_vertex() == h.max_degree_vertex()
+    del torch
+
+
+def test_device_graph_walk_and_validator():
+    import ctypes
+
+    import torch
+
+    from paper_2404_08364_b200 import _lib
+    d = rmat.rmat_graph_device(15)
+    h = d.to_host()
+    n = d.vertex_count
+    starts = torch.arange(n, dtype=torch.int64, device="cuda")
+    L = 40
+    seq = torch.empty(n * L, dtype=torch.int32, device="cuda")
+    ln = torch.empty(n, dtype=torch.int32, device="cuda")
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    app = fw.AppConfig(app="node2vec", length=L)
+    eng = fw.EngineConfig()
+    from paper_2404_08364_b200.engine import _fw_structs
+    a, e, _s = _fw_structs(app, eng)
+    lib = _lib.load()
+    stream = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.fw_walk_device(d.handle(0).ptr, starts.data_ptr(), n, 0, ctypes.byref(a),
+                                  ctypes.byref(e), 0, seq.data_ptr(), ln.data_ptr(),
+                                  stats.data_ptr(), stream))
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(lib.fw_validate_device(d.handle(0).ptr, starts.data_ptr(), n, seq.data_ptr(),
+                                      ln.data_ptr(), L, None, 0, bad.data_ptr(), stream))
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
+    oseq, oln, ost = oracle.walk(h.offsets, h.targets, h.weights, h.labels,
+                                 np.arange(n), app="node2vec", length=L)
+    np.testing.assert_array_equal(ln.cpu().numpy().view(np.uint32), oln)
+    np.testing.assert_array_equal(seq.cpu().numpy().view(np.uint32).reshape(n, L), oseq)
+    st = stats.cpu().numpy()
+    assert st[:6].tolist() == ost.tolist()
+    assert st[6] == int(oln.sum())
+    # corrupt one step: the GPU validator must see it
+    s2 = seq.view(n, L).clone()
+    i = int(np.flatnonzero(oln >= 3)[0])
+    s2[i, 2] = int(s2[i, 2].item() == 0)
+    bad.zero_()
+    _lib.check(lib.fw_validate_device(d.handle(0).ptr, starts.data_ptr(), n, s2.data_ptr(),
+                                      ln.data_ptr(), L, None, 0, bad.data_ptr(), stream))
+    torch.cuda.synchronize()
+    assert int(bad.item()) >= 0  # may be a real edge by chance; checked exactly below
+    want = oracle.validate(h.offsets, h.targets, h.labels, np.arange(n),
+                           s2.cpu().numpy().view(np.uint32), oln)
+    assert int(bad.item()) == want
+
+
+def test_split_across_device_handles(golden):
+    """EngineConfig.devices: the query range is split across graph replicas;
+    global qids keep the result identical (here two replicas on one GPU)."""
+    g = _graph(golden, "rmat12")
+    starts = golden.starts("n2v_rmat12")
+    eng = fw.EngineConfig(replay=True, devices=(0, 0, 0))
+    seq, ln, st = _run(g, starts, fw.AppConfig(app="node2vec", length=24), eng, 0)
+    want_seq, want_len, want_stats = golden.expected("n2v_rmat12")
+    np.testing.assert_array_equal(seq, want_seq)
+    np.testing.assert_array_equal(ln, want_len)
+    assert [getattr(st, f) for f in STAT_NAMES] == want_stats.tolist()
+
+
+def test_base_qid_window_equals_slice(s16):
+    """A query recomputed from its global qid equals its slot in a full run
+    (replay makes a walk a pure function of the global qid)."""
+    g = s16
+    starts = np.arange(4096, dtype=np.int64)
+    app = fw.AppConfig(app="node2vec", length=30)
+    full, fl, _ = _run(g, starts, app, fw.EngineConfig(replay=True), 3)
+    budget = fw.EngineConfig(replay=True, memory_budget=2 * 31 * 4 * 1000, graph_bytes=0)
+    part, pl, st = _run(g, starts, app, budget, 3)
+    assert st.batches == 5
+    np.testing.assert_array_equal(part, full)
+    np.testing.assert_array_equal(pl, fl)
+
+
+def test_errors_raise_before_kernel(s16):
+    with pytest.raises(fw.ValidationError):
+        list(fw.run_batches(s16, np.array([s16.vertex_count]), fw.AppConfig(),
+                            fw.EngineConfig()))
+    with pytest.raises(fw.ConfigError):
+        list(fw.run_batches(s16, np.array([0]), fw.AppConfig(length=1 << 20),
+                            fw.EngineConfig()))
+    with pytest.raises(fw.ConfigError):
+        fw.EngineConfig(k_big=1001).validate()

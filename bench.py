@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--nq", type=int, default=0, help="queries per GPU (0 = one per vertex)")
     return p.parse_args()
 
 
@@ -299,9 +300,9 @@ def bench_ours(args):
             dg = DeviceGraph(V, E_, *arrs[:3], arrs[3] if labels else None, device=local)
     handle = dg.handle(local).ptr
     hub = dg.max_degree_vertex()
-    n = V
+    n = args.nq if args.nq else V
     base_qid = rank * n
-    starts_h = make_starts(args, n, hub)
+    starts_h = make_starts(args, V, hub)[:n]
     starts = torch.from_numpy(starts_h).to(dev)
     L = app.length
     seq = torch.empty(n * L, dtype=torch.int32, device=dev)

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -375,6 +376,10 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     a.k_big = eng->k_big;
     a.d_t = eng->d_t;
     a.h = mix64(seed + GOLDEN);
+    {
+        const char *mr = getenv("FW_MERGE_RATIO");
+        a.merge_ratio = mr ? (uint32_t)atoi(mr) : 4u;
+    }
     a.stats = (long long *)d_stats;
     unsigned slot;
     {

@@ -190,6 +190,109 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
     return __reduce_max_sync(FULL, cand);
 }
 
+// ---------------------------------------------------------------------------
+// Node2Vec DPRS, exact order, prev >= 0: the hot path of the headline config.
+// Membership of u = targets[elo+i] in N(prev) (_kernels.py:288-306) is
+// decided by a warp merge: N(cur) is sorted, so tile after tile the lanes'
+// u values only increase; a 32-entry window of N(prev) lives in registers
+// (lane j holds P[wpos+j]) and each lane runs a 5-step lower_bound over it
+// with shuffles.  The window only moves forward, so a step reads N(prev)
+// once, coalesced (4*d_prev bytes, the algorithmic count) instead of
+// d_cur*log2(d_prev) dependent probes.  When d_prev >> d_cur the merge would
+// stream far more of N(prev) than the probes touch, so the per-lane binary
+// search is kept (s.merge == false).  The selected target is carried with
+// the candidate, so no dependent reload of targets[elo+sel-1] is needed.
+// ---------------------------------------------------------------------------
+struct N2VWin {
+    const uint32_t *P;  // N(prev)
+    uint32_t dp;        // d(prev)
+    uint32_t wpos;      // window start
+    uint32_t pw;        // this lane's window entry (0xFFFFFFFF past the end)
+    bool wend;          // window covers the end of N(prev)
+    bool merge;
+};
+
+__device__ __forceinline__ bool n2v_member(const WalkArgs &a, const StepCtx &s, N2VWin &W,
+                                           uint32_t u, bool need, int lane) {
+    if (!W.merge) return need && in_sorted(a.tgt, s.plo, s.phi, u);
+    bool res = !need, mem = false;
+    for (;;) {
+        const uint32_t wmax = __shfl_sync(FULL, W.pw, 31);
+        const bool here = !res && (u <= wmax || W.wend);
+        int pos = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t v = __shfl_sync(FULL, W.pw, pos + step - 1);
+            if (v < u) pos += step;
+        }
+        const uint32_t v = __shfl_sync(FULL, W.pw, pos);
+        if (here) {
+            mem = v == u;
+            res = true;
+        }
+        if (__all_sync(FULL, res)) break;
+        W.wpos += 32;
+        W.pw = W.wpos + lane < W.dp ? ldg(W.P + W.wpos + lane) : 0xFFFFFFFFu;
+        W.wend = W.wpos + 32 >= W.dp;
+    }
+    return mem;
+}
+
+template <int KMODE>  // 1: k == 32, 2: k == 256, 0: any k
+__device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
+                                   uint32_t &sel_u) {
+    const uint32_t deg = s.deg;
+    N2VWin W;
+    W.P = a.tgt + s.plo;
+    W.dp = (uint32_t)(s.phi - s.plo);
+    W.merge = W.dp <= a.merge_ratio * deg + 32;
+    W.wpos = 0;
+    W.pw = (W.merge && (uint32_t)lane < W.dp) ? ldg(W.P + lane) : 0xFFFFFFFFu;
+    W.wend = W.dp <= 32;
+    const uint32_t prev = (uint32_t)s.prev;
+    double carry = 0.0;
+    uint32_t cand = 0, cand_u = 0;
+    uint64_t base[KMODE == 2 ? 8 : 1];
+    if constexpr (KMODE == 1) base[0] = lane_base(a, s, lane);
+    if constexpr (KMODE == 2) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) base[q] = lane_base(a, s, q * 32 + lane);
+    }
+    uint64_t cadd = 0;  // chunk counter * GOLDEN
+    for (uint32_t c0 = 0; c0 < deg; c0 += (KMODE == 2 ? 256 : 32)) {
+#pragma unroll
+        for (int q = 0; q < (KMODE == 2 ? 8 : 1); q++) {
+            const uint32_t t0 = c0 + q * 32;
+            if (t0 < deg) {  // warp-uniform
+                const uint32_t i = t0 + lane;
+                const bool valid = i < deg;
+                const uint32_t u = valid ? ldg(a.tgt + s.elo + i) : 0xFFFFFFFFu;
+                const float wf = (valid && a.weighted) ? ldg(a.w + s.elo + i) : 1.0f;
+                const bool isprev = valid && u == prev;
+                const bool mem = n2v_member(a, s, W, u, valid && !isprev, lane);
+                const double bse = isprev ? a.inv_a : (mem ? 1.0 : a.inv_b);
+                const double wv = valid ? (a.weighted ? __dmul_rn(bse, (double)wf) : bse) : 0.0;
+                const double incl = warp_incl_scan(wv, lane);
+                const double P = __dadd_rn(carry, incl);
+                double r;
+                if constexpr (KMODE == 1) r = u01_word(base[0] + cadd);
+                else if constexpr (KMODE == 2) r = u01_word(base[q] + cadd);
+                else r = u01(lane_base(a, s, i % k), (uint64_t)(i / k));
+                if (wv > 0.0 && __dmul_rn(r, P) < wv) {
+                    cand = i + 1;
+                    cand_u = u;
+                }
+                carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
+            }
+        }
+        cadd += GOLDEN;
+    }
+    const uint32_t sel = __reduce_max_sync(FULL, cand);
+    const unsigned who = __ballot_sync(FULL, cand == sel);
+    sel_u = __shfl_sync(FULL, cand_u, __ffs(who) - 1);
+    return sel;
+}
+
 template <int APP>
 __device__ uint32_t dprs_warp_ordered(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane) {
     const uint32_t deg = s.deg;
@@ -222,7 +325,7 @@ __device__ uint32_t dprs_warp_ordered(const WalkArgs &a, const StepCtx &s, uint3
 // The persistent walker.
 // ---------------------------------------------------------------------------
 template <int APP, int SAMPLER, bool EXACT>
-__global__ void __launch_bounds__(kWalkThreads)
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks)
 walk_kernel(const WalkArgs a) {
     const int lane = threadIdx.x & 31;
     long long st[ST_COUNT];
@@ -272,9 +375,23 @@ walk_kernel(const WalkArgs a) {
             }
             const uint32_t chunks = (s.deg - 1) / k + 1;
             uint32_t sel;
+            uint32_t sel_u = 0;
+            bool have_u = false;
             if constexpr (SAMPLER == SAMPLER_DPRS) {
-                if constexpr (EXACT) sel = dprs_warp_exact<APP>(a, s, k, lane);
-                else sel = dprs_warp_ordered<APP>(a, s, k, lane);
+                if constexpr (EXACT && APP == APP_NODE2VEC) {
+                    if (s.prev >= 0) {
+                        if (k == 32) sel = dprs_n2v_exact<1>(a, s, k, lane, sel_u);
+                        else if (k == 256) sel = dprs_n2v_exact<2>(a, s, k, lane, sel_u);
+                        else sel = dprs_n2v_exact<0>(a, s, k, lane, sel_u);
+                        have_u = true;
+                    } else {
+                        sel = dprs_warp_exact<APP>(a, s, k, lane);
+                    }
+                } else if constexpr (EXACT) {
+                    sel = dprs_warp_exact<APP>(a, s, k, lane);
+                } else {
+                    sel = dprs_warp_ordered<APP>(a, s, k, lane);
+                }
                 st[ST_COLLECTIVES] += 2 * chunks;
                 st[ST_EDGES] += s.deg;
             } else {
@@ -285,7 +402,7 @@ walk_kernel(const WalkArgs a) {
             st[ST_DRAWS] += (long long)chunks * k;
             st[ST_BYTES] += (APP == APP_METAPATH ? 9 : 8) * s.deg;
             if (sel == 0) break;
-            const uint32_t u = ldg(a.tgt + s.elo + sel - 1);
+            const uint32_t u = have_u ? sel_u : ldg(a.tgt + s.elo + sel - 1);
             if (lane == (int)(step & 31)) pathbuf = u;
             emitted = (uint32_t)step + 1;
             st[ST_BYTES] += 4;

@@ -5,6 +5,10 @@
 namespace fw {
 
 constexpr int kWalkThreads = 256;  // 8 warp walkers per CTA
+#ifndef FW_MIN_BLOCKS
+#define FW_MIN_BLOCKS 4
+#endif
+constexpr int kWalkMinBlocks = FW_MIN_BLOCKS;  // >= 32 resident warps per SM
 
 // Kernel arguments (passed by value through the constant bank).
 struct WalkArgs {
@@ -24,6 +28,7 @@ struct WalkArgs {
     double stop_prob, inv_a, inv_b;
     int64_t k_small, k_big, d_t;
     uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
+    uint32_t merge_ratio;  // node2vec: merge N(prev) when d_prev <= ratio*d_cur + 32
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };

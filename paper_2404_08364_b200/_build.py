@@ -33,14 +33,15 @@ def needs_build():
     return any(os.path.getmtime(os.path.join(_HERE, s)) > t for s in SOURCES + HEADERS)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, out=None, extra=()):
+    out = out or OUT
+    if not force and out == OUT and not needs_build():
         return OUT
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", OUT, *[os.path.join(_HERE, s) for s in SOURCES]]
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", out, *[os.path.join(_HERE, s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=_HERE)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libflowwalk.so")
+LIB_PATH = os.environ.get("FW_LIB_PATH") or os.path.join(_HERE, "libflowwalk.so")
 
 FW_OK, FW_EVALIDATION, FW_ECONFIG, FW_ECUDA, FW_ENOMEM = range(5)
 ORDER_AUTO, ORDER_SEQUENTIAL = 0, 1

@@ -241,7 +241,12 @@ __device__ __forceinline__ bool n2v_member(const WalkArgs &a, const StepCtx &s, 
 template <int KMODE>  // 1: k == 32, 2: k == 256, 0: any k
 __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                    uint32_t &sel_u) {
+    // Tiles of 32 elements in natural order; the targets/weights of the next
+    // kPf tiles are in flight while a tile is processed (the step is
+    // latency-bound without it: one DRAM round trip per tile).
+    constexpr int kPf = 8;  // == tiles per k=256 chunk, so tile % 8 is static
     const uint32_t deg = s.deg;
+    const uint32_t ntiles = (deg + 31) >> 5;
     N2VWin W;
     W.P = a.tgt + s.plo;
     W.dp = (uint32_t)(s.phi - s.plo);
@@ -250,6 +255,16 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
     W.pw = (W.merge && (uint32_t)lane < W.dp) ? ldg(W.P + lane) : 0xFFFFFFFFu;
     W.wend = W.dp <= 32;
     const uint32_t prev = (uint32_t)s.prev;
+    const uint32_t *tg = a.tgt + s.elo;
+    const float *wt = a.w + s.elo;
+    uint32_t pu[kPf];
+    float pf[kPf];
+#pragma unroll
+    for (int d = 0; d < kPf; d++) {
+        const uint32_t i = d * 32 + lane;
+        pu[d] = i < deg ? ldg(tg + i) : 0xFFFFFFFFu;
+        pf[d] = (i < deg && a.weighted) ? ldg(wt + i) : 1.0f;
+    }
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
     uint64_t base[KMODE == 2 ? 8 : 1];
@@ -258,16 +273,20 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
 #pragma unroll
         for (int q = 0; q < 8; q++) base[q] = lane_base(a, s, q * 32 + lane);
     }
-    uint64_t cadd = 0;  // chunk counter * GOLDEN
-    for (uint32_t c0 = 0; c0 < deg; c0 += (KMODE == 2 ? 256 : 32)) {
+    for (uint32_t g = 0; g < ntiles; g += kPf) {
 #pragma unroll
-        for (int q = 0; q < (KMODE == 2 ? 8 : 1); q++) {
-            const uint32_t t0 = c0 + q * 32;
-            if (t0 < deg) {  // warp-uniform
-                const uint32_t i = t0 + lane;
+        for (int d = 0; d < kPf; d++) {
+            const uint32_t t = g + d;
+            if (t < ntiles) {  // warp-uniform
+                const uint32_t i = t * 32 + lane;
                 const bool valid = i < deg;
-                const uint32_t u = valid ? ldg(a.tgt + s.elo + i) : 0xFFFFFFFFu;
-                const float wf = (valid && a.weighted) ? ldg(a.w + s.elo + i) : 1.0f;
+                const uint32_t u = pu[d];
+                const float wf = pf[d];
+                {  // refill this slot with tile t + kPf
+                    const uint32_t i2 = i + kPf * 32;
+                    pu[d] = i2 < deg ? ldg(tg + i2) : 0xFFFFFFFFu;
+                    pf[d] = (i2 < deg && a.weighted) ? ldg(wt + i2) : 1.0f;
+                }
                 const bool isprev = valid && u == prev;
                 const bool mem = n2v_member(a, s, W, u, valid && !isprev, lane);
                 const double bse = isprev ? a.inv_a : (mem ? 1.0 : a.inv_b);
@@ -275,8 +294,8 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
                 const double incl = warp_incl_scan(wv, lane);
                 const double P = __dadd_rn(carry, incl);
                 double r;
-                if constexpr (KMODE == 1) r = u01_word(base[0] + cadd);
-                else if constexpr (KMODE == 2) r = u01_word(base[q] + cadd);
+                if constexpr (KMODE == 1) r = u01_word(base[0] + (uint64_t)t * GOLDEN);
+                else if constexpr (KMODE == 2) r = u01_word(base[d] + (uint64_t)(t >> 3) * GOLDEN);
                 else r = u01(lane_base(a, s, i % k), (uint64_t)(i / k));
                 if (wv > 0.0 && __dmul_rn(r, P) < wv) {
                     cand = i + 1;
@@ -285,7 +304,6 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
                 carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
             }
         }
-        cadd += GOLDEN;
     }
     const uint32_t sel = __reduce_max_sync(FULL, cand);
     const unsigned who = __ballot_sync(FULL, cand == sel);

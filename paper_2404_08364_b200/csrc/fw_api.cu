@@ -212,8 +212,8 @@ extern "C" int fw_graph_create(const int64_t *offsets, const uint32_t *targets,
     };
     cudaError_t e;
     if ((e = cudaMalloc(&g->off, (V + 1) * sizeof(int64_t))) != cudaSuccess ||
-        (e = cudaMalloc(&g->tgt, std::max<uint64_t>(E, 1) * sizeof(uint32_t))) != cudaSuccess ||
-        (e = cudaMalloc(&g->w, std::max<uint64_t>(E, 1) * sizeof(float))) != cudaSuccess ||
+        (e = cudaMalloc(&g->tgt, (E + 4) * sizeof(uint32_t))) != cudaSuccess ||  // +4: tail of
+        (e = cudaMalloc(&g->w, (E + 4) * sizeof(float))) != cudaSuccess ||        // 16-byte tiles
         (labels && (e = cudaMalloc(&g->lab, std::max<uint64_t>(E, 1))) != cudaSuccess))
         return fail(set_err(FW_ENOMEM, "graph allocation: %s", cudaGetErrorString(e)));
     const size_t chunk = 64u << 20;
@@ -378,7 +378,7 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     a.h = mix64(seed + GOLDEN);
     {
         const char *mr = getenv("FW_MERGE_RATIO");
-        a.merge_ratio = mr ? (uint32_t)atoi(mr) : 4u;
+        a.merge_ratio = mr ? (uint32_t)atoi(mr) : 32u;
     }
     a.stats = (long long *)d_stats;
     unsigned slot;

@@ -192,122 +192,216 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
 
 // ---------------------------------------------------------------------------
 // Node2Vec DPRS, exact order, prev >= 0: the hot path of the headline config.
-// Membership of u = targets[elo+i] in N(prev) (_kernels.py:288-306) is
-// decided by a warp merge: N(cur) is sorted, so tile after tile the lanes'
-// u values only increase; a 32-entry window of N(prev) lives in registers
-// (lane j holds P[wpos+j]) and each lane runs a 5-step lower_bound over it
-// with shuffles.  The window only moves forward, so a step reads N(prev)
-// once, coalesced (4*d_prev bytes, the algorithmic count) instead of
-// d_cur*log2(d_prev) dependent probes.  When d_prev >> d_cur the merge would
-// stream far more of N(prev) than the probes touch, so the per-lane binary
-// search is kept (s.merge == false).  The selected target is carried with
-// the candidate, so no dependent reload of targets[elo+sel-1] is needed.
+//
+// Layout: tiles of 128 elements of N(cur), lane p holding 4 consecutive
+// elements (16-byte loads of targets and weights; the tile grid is anchored
+// at elo & ~3 and out-of-range slots are masked), so the natural-order fp64
+// prefix is a 4-element local prefix plus one warp scan per 128 elements.
+// The next tile is loaded while the current one is processed.
+//
+// Membership u in N(prev) (_kernels.py:288-306): N(prev) is sorted and the
+// u values only grow along N(cur), so N(prev) is consumed in chunks of up to
+// kChunk entries, each hashed into a per-warp open-addressing table in
+// shared memory; a lane looks u up when u <= max(chunk) (or the chunk is the
+// last one), otherwise the window advances (skipping chunks whose max is
+// below every pending u).  N(prev) is read once, coalesced.  When d(prev) is
+// far larger than d(cur) a per-element branchless binary search in global
+// memory is cheaper and is used instead.
+//
+// Random draws: element i uses logical lane j = i mod k and counter i div k;
+// for power-of-two k <= 256 the k lane bases are staged in shared memory.
+// The selected target travels with the candidate (no dependent reload).
 // ---------------------------------------------------------------------------
-struct N2VWin {
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+struct HashWin {
     const uint32_t *P;  // N(prev)
+    uint32_t *tab;      // per-warp table (kHashSlots)
     uint32_t dp;        // d(prev)
-    uint32_t wpos;      // window start
-    uint32_t pw;        // this lane's window entry (0xFFFFFFFF past the end)
-    bool wend;          // window covers the end of N(prev)
-    bool merge;
+    uint32_t c0, cn;    // current chunk [c0, c0+cn)
+    uint32_t cmax;      // P[c0+cn-1]
+    uint32_t hshift;    // 32 - log2(table size)
+    uint32_t hmask;
+    bool last;          // chunk reaches the end of N(prev)
 };
 
-__device__ __forceinline__ bool n2v_member(const WalkArgs &a, const StepCtx &s, N2VWin &W,
-                                           uint32_t u, bool need, int lane) {
-    if (!W.merge) return need && in_sorted(a.tgt, s.plo, s.phi, u);
-    bool res = !need, mem = false;
-    for (;;) {
-        const uint32_t wmax = __shfl_sync(FULL, W.pw, 31);
-        const bool here = !res && (u <= wmax || W.wend);
-        int pos = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            const uint32_t v = __shfl_sync(FULL, W.pw, pos + step - 1);
-            if (v < u) pos += step;
-        }
-        const uint32_t v = __shfl_sync(FULL, W.pw, pos);
-        if (here) {
-            mem = v == u;
-            res = true;
-        }
-        if (__all_sync(FULL, res)) break;
-        W.wpos += 32;
-        W.pw = W.wpos + lane < W.dp ? ldg(W.P + W.wpos + lane) : 0xFFFFFFFFu;
-        W.wend = W.wpos + 32 >= W.dp;
-    }
-    return mem;
+__device__ __forceinline__ uint32_t hslot(uint32_t u, uint32_t shift) {
+    return (u * 0x9E3779B1u) >> shift;
 }
 
-template <int KMODE>  // 1: k == 32, 2: k == 256, 0: any k
-__device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
-                                   uint32_t &sel_u) {
-    // Tiles of 32 elements in natural order; the targets/weights of the next
-    // kPf tiles are in flight while a tile is processed (the step is
-    // latency-bound without it: one DRAM round trip per tile).
-    constexpr int kPf = 8;  // == tiles per k=256 chunk, so tile % 8 is static
-    const uint32_t deg = s.deg;
-    const uint32_t ntiles = (deg + 31) >> 5;
-    N2VWin W;
-    W.P = a.tgt + s.plo;
-    W.dp = (uint32_t)(s.phi - s.plo);
-    W.merge = W.dp <= a.merge_ratio * deg + 32;
-    W.wpos = 0;
-    W.pw = (W.merge && (uint32_t)lane < W.dp) ? ldg(W.P + lane) : 0xFFFFFFFFu;
-    W.wend = W.dp <= 32;
-    const uint32_t prev = (uint32_t)s.prev;
-    const uint32_t *tg = a.tgt + s.elo;
-    const float *wt = a.w + s.elo;
-    uint32_t pu[kPf];
-    float pf[kPf];
+// (Re)build the table from P[c0, c0 + min(kChunk, dp - c0)).
+__device__ __forceinline__ void hash_build(HashWin &H, int lane) {
+    H.cn = min(kChunk, H.dp - H.c0);
+    uint32_t bits = 6;
+    while ((1u << bits) < 2 * H.cn) bits++;
+    const uint32_t size = 1u << bits;
+    H.hshift = 32 - bits;
+    H.hmask = size - 1;
+    __syncwarp();
+    for (uint32_t x = lane * 4; x < size; x += 128)
+        *reinterpret_cast<uint4 *>(H.tab + x) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    __syncwarp();
+    const uint32_t *src = H.P + H.c0;
+    for (uint32_t x = lane; x < H.cn; x += 32) {
+        const uint32_t key = ldg(src + x);
+        uint32_t sl = hslot(key, H.hshift);
+        for (;;) {
+            const uint32_t old = atomicCAS(H.tab + sl, kEmpty, key);
+            if (old == kEmpty || old == key) break;
+            sl = (sl + 1) & H.hmask;
+        }
+    }
+    H.cmax = ldg(src + H.cn - 1);
+    H.last = H.c0 + H.cn >= H.dp;
+    __syncwarp();
+}
+
+__device__ __forceinline__ bool hash_probe(const HashWin &H, uint32_t u) {
+    uint32_t sl = hslot(u, H.hshift);
+    for (;;) {
+        const uint32_t key = H.tab[sl];
+        if (key == u) return true;
+        if (key == kEmpty) return false;
+        sl = (sl + 1) & H.hmask;
+    }
+}
+
+// Membership for the 4 elements of this lane (need[e] masks them).
+__device__ __forceinline__ void member4_hash(HashWin &H, const uint32_t u[4], bool need[4],
+                                            bool mem[4], int lane) {
+    for (;;) {
+        bool pending = false;
 #pragma unroll
-    for (int d = 0; d < kPf; d++) {
-        const uint32_t i = d * 32 + lane;
-        pu[d] = i < deg ? ldg(tg + i) : 0xFFFFFFFFu;
-        pf[d] = (i < deg && a.weighted) ? ldg(wt + i) : 1.0f;
+        for (int e = 0; e < 4; e++) {
+            if (need[e]) {
+                if (u[e] <= H.cmax || H.last) {
+                    mem[e] = hash_probe(H, u[e]);
+                    need[e] = false;
+                } else {
+                    pending = true;
+                }
+            }
+        }
+        if (!__any_sync(FULL, pending)) return;
+        uint32_t umin = kEmpty;
+#pragma unroll
+        for (int e = 3; e >= 0; e--)
+            if (need[e]) umin = u[e];
+        umin = __reduce_min_sync(FULL, umin);
+        // advance: skip whole chunks that end below every pending u
+        uint32_t c0 = H.c0 + H.cn;
+        while (c0 + kChunk < H.dp && ldg(H.P + c0 + kChunk - 1) < umin) c0 += kChunk;
+        H.c0 = c0;
+        hash_build(H, lane);
+    }
+}
+
+// 4 independent branchless binary searches over P[0, dp) (global memory).
+__device__ __forceinline__ void member4_bsearch(const uint32_t *__restrict__ P, uint32_t dp,
+                                               const uint32_t u[4], const bool need[4],
+                                               bool mem[4]) {
+    uint32_t b[4] = {0, 0, 0, 0};
+    uint32_t n = dp;
+    while (n > 1) {
+        const uint32_t half = n >> 1;
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            b[e] = ldg(P + b[e] + half) <= u[e] ? b[e] + half : b[e];
+        n -= half;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) mem[e] = need[e] && dp > 0 && ldg(P + b[e]) == u[e];
+}
+
+__device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
+                                   uint32_t *wsm, uint32_t &sel_u) {
+    const uint32_t deg = s.deg;
+    const uint32_t prev = (uint32_t)s.prev;
+    // lane bases (power-of-two k <= 256) -> shared memory
+    uint64_t *sb = reinterpret_cast<uint64_t *>(wsm + kHashSlots);
+    const bool kpow2 = k <= 256 && (k & (k - 1)) == 0;
+    const uint32_t kshift = 31 - __clz(k), kmask = k - 1;
+    if (kpow2) {
+        const uint32_t nl = min(k, deg);
+        for (uint32_t j = lane; j < nl; j += 32) sb[j] = lane_base(a, s, j);
+    }
+    HashWin H;
+    H.P = a.tgt + s.plo;
+    H.tab = wsm;
+    H.dp = (uint32_t)(s.phi - s.plo);
+    const bool use_hash = H.dp <= a.merge_ratio * deg + 2 * kChunk;
+    if (use_hash) {
+        H.c0 = 0;
+        hash_build(H, lane);  // (ends with __syncwarp: sb[] visible too)
+    } else {
+        __syncwarp();
+    }
+    const uint32_t off = (uint32_t)(s.elo & 3);
+    const uint32_t span = deg + off;
+    const uint32_t ntiles = (span + 127) >> 7;
+    const uint4 *T4 = reinterpret_cast<const uint4 *>(a.tgt + (s.elo - off));
+    const float4 *W4 = reinterpret_cast<const float4 *>(a.w + (s.elo - off));
+    uint4 nu = make_uint4(0, 0, 0, 0);
+    float4 nw = make_float4(1.f, 1.f, 1.f, 1.f);
+    if ((uint32_t)lane * 4 < span) {
+        nu = ldg(T4 + lane);
+        if (a.weighted) nw = ldg(W4 + lane);
     }
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
-    uint64_t base[KMODE == 2 ? 8 : 1];
-    if constexpr (KMODE == 1) base[0] = lane_base(a, s, lane);
-    if constexpr (KMODE == 2) {
+    for (uint32_t t = 0; t < ntiles; t++) {
+        const uint4 u4 = nu;
+        const float4 w4 = nw;
+        const uint32_t nx = (t + 1) * 128 + lane * 4;
+        if (nx < span) {  // prefetch the next tile
+            nu = ldg(T4 + (nx >> 2));
+            if (a.weighted) nw = ldg(W4 + (nx >> 2));
+        }
+        const int32_t i0 = (int32_t)(t * 128 + lane * 4) - (int32_t)off;
+        const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
+        const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
+        bool valid[4], need[4], mem[4] = {false, false, false, false};
 #pragma unroll
-        for (int q = 0; q < 8; q++) base[q] = lane_base(a, s, q * 32 + lane);
-    }
-    for (uint32_t g = 0; g < ntiles; g += kPf) {
+        for (int e = 0; e < 4; e++) {
+            valid[e] = i0 + e >= 0 && i0 + e < (int32_t)deg;
+            need[e] = valid[e] && u[e] != prev;
+        }
+        if (use_hash) member4_hash(H, u, need, mem, lane);
+        else member4_bsearch(H.P, H.dp, u, need, mem);
+        double wv[4], pre[4];
 #pragma unroll
-        for (int d = 0; d < kPf; d++) {
-            const uint32_t t = g + d;
-            if (t < ntiles) {  // warp-uniform
-                const uint32_t i = t * 32 + lane;
-                const bool valid = i < deg;
-                const uint32_t u = pu[d];
-                const float wf = pf[d];
-                {  // refill this slot with tile t + kPf
-                    const uint32_t i2 = i + kPf * 32;
-                    pu[d] = i2 < deg ? ldg(tg + i2) : 0xFFFFFFFFu;
-                    pf[d] = (i2 < deg && a.weighted) ? ldg(wt + i2) : 1.0f;
-                }
-                const bool isprev = valid && u == prev;
-                const bool mem = n2v_member(a, s, W, u, valid && !isprev, lane);
-                const double bse = isprev ? a.inv_a : (mem ? 1.0 : a.inv_b);
-                const double wv = valid ? (a.weighted ? __dmul_rn(bse, (double)wf) : bse) : 0.0;
-                const double incl = warp_incl_scan(wv, lane);
-                const double P = __dadd_rn(carry, incl);
-                double r;
-                if constexpr (KMODE == 1) r = u01_word(base[0] + (uint64_t)t * GOLDEN);
-                else if constexpr (KMODE == 2) r = u01_word(base[d] + (uint64_t)(t >> 3) * GOLDEN);
-                else r = u01(lane_base(a, s, i % k), (uint64_t)(i / k));
-                if (wv > 0.0 && __dmul_rn(r, P) < wv) {
+        for (int e = 0; e < 4; e++) {
+            const double bse = u[e] == prev ? a.inv_a : (mem[e] ? 1.0 : a.inv_b);
+            wv[e] = valid[e] ? (a.weighted ? __dmul_rn(bse, (double)wf[e]) : bse) : 0.0;
+        }
+        pre[0] = wv[0];
+        pre[1] = __dadd_rn(pre[0], wv[1]);
+        pre[2] = __dadd_rn(pre[1], wv[2]);
+        pre[3] = __dadd_rn(pre[2], wv[3]);
+        const double incl = warp_incl_scan(pre[3], lane);
+        const double excl = __shfl_up_sync(FULL, incl, 1);
+        const double base = __dadd_rn(carry, lane == 0 ? 0.0 : excl);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            if (wv[e] > 0.0) {
+                const uint32_t i = (uint32_t)(i0 + e);
+                uint64_t word;
+                if (kpow2) word = sb[i & kmask] + (uint64_t)(i >> kshift) * GOLDEN;
+                else word = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
+                const double r = u01_word(word);
+                const double P = __dadd_rn(base, pre[e]);
+                if (__dmul_rn(r, P) < wv[e]) {
                     cand = i + 1;
-                    cand_u = u;
+                    cand_u = u[e];
                 }
-                carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
             }
         }
+        carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
     }
     const uint32_t sel = __reduce_max_sync(FULL, cand);
     const unsigned who = __ballot_sync(FULL, cand == sel);
     sel_u = __shfl_sync(FULL, cand_u, __ffs(who) - 1);
+    __syncwarp();  // the table is rebuilt by the next step
     return sel;
 }
 
@@ -346,6 +440,8 @@ template <int APP, int SAMPLER, bool EXACT>
 __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks)
 walk_kernel(const WalkArgs a) {
     const int lane = threadIdx.x & 31;
+    extern __shared__ __align__(16) uint32_t fw_smem[];
+    uint32_t *wsm = fw_smem + (threadIdx.x >> 5) * kWarpSmemWords;
     long long st[ST_COUNT];
 #pragma unroll
     for (int i = 0; i < ST_COUNT; i++) st[i] = 0;
@@ -360,7 +456,7 @@ walk_kernel(const WalkArgs a) {
         StepCtx s;
         int64_t cur = ldg(a.starts + qi);
         s.prev = -1;
-        int64_t pdeg = 0;
+        int64_t pdeg = 0, pelo = 0;
         uint32_t emitted = 0;
         uint32_t pathbuf = 0xFFFFFFFFu;  // lane (t & 31) holds step t of the open 32-block
         for (;;) {
@@ -385,9 +481,9 @@ walk_kernel(const WalkArgs a) {
                 s.want = ldg(a.schema + step);
             }
             if constexpr (APP == APP_NODE2VEC) {
-                if (s.prev >= 0) {
-                    s.plo = ldg(a.off + s.prev);
-                    s.phi = ldg(a.off + s.prev + 1);
+                if (s.prev >= 0) {  // N(prev) = the previous step's N(cur)
+                    s.plo = pelo;
+                    s.phi = pelo + pdeg;
                     st[ST_BYTES] += 16 + 4 * pdeg;
                 }
             }
@@ -398,9 +494,7 @@ walk_kernel(const WalkArgs a) {
             if constexpr (SAMPLER == SAMPLER_DPRS) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
-                        if (k == 32) sel = dprs_n2v_exact<1>(a, s, k, lane, sel_u);
-                        else if (k == 256) sel = dprs_n2v_exact<2>(a, s, k, lane, sel_u);
-                        else sel = dprs_n2v_exact<0>(a, s, k, lane, sel_u);
+                        sel = dprs_n2v_exact(a, s, k, lane, wsm, sel_u);
                         have_u = true;
                     } else {
                         sel = dprs_warp_exact<APP>(a, s, k, lane);
@@ -426,6 +520,7 @@ walk_kernel(const WalkArgs a) {
             st[ST_BYTES] += 4;
             s.prev = cur;
             pdeg = s.deg;
+            pelo = s.elo;
             cur = (int64_t)u;
             if ((emitted & 31) == 0) {
                 row[emitted - 32 + lane] = pathbuf;
@@ -453,7 +548,7 @@ walk_kernel(const WalkArgs a) {
 
 template <int APP, int SAMPLER, bool EXACT>
 static cudaError_t launch_t(const WalkArgs &a, int grid, cudaStream_t stream) {
-    walk_kernel<APP, SAMPLER, EXACT><<<grid, kWalkThreads, 0, stream>>>(a);
+    walk_kernel<APP, SAMPLER, EXACT><<<grid, kWalkThreads, kWalkSmemBytes, stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -461,7 +556,7 @@ template <int APP, int SAMPLER, bool EXACT>
 static int occupancy_t() {
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_kernel<APP, SAMPLER, EXACT>,
-                                                  kWalkThreads, 0);
+                                                  kWalkThreads, kWalkSmemBytes);
     return nb;
 }
 

@@ -9,6 +9,11 @@ constexpr int kWalkThreads = 256;  // 8 warp walkers per CTA
 #define FW_MIN_BLOCKS 4
 #endif
 constexpr int kWalkMinBlocks = FW_MIN_BLOCKS;  // >= 32 resident warps per SM
+// per-warp shared memory: N(prev) hash window + 256 staged lane bases
+constexpr uint32_t kHashSlots = 1024;
+constexpr uint32_t kChunk = 512;  // N(prev) entries hashed at a time (load <= 1/2)
+constexpr uint32_t kWarpSmemWords = kHashSlots + 2 * 256;
+constexpr int kWalkSmemBytes = (kWalkThreads / 32) * kWarpSmemWords * 4;
 
 // Kernel arguments (passed by value through the constant bank).
 struct WalkArgs {
@@ -28,7 +33,7 @@ struct WalkArgs {
     double stop_prob, inv_a, inv_b;
     int64_t k_small, k_big, d_t;
     uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
-    uint32_t merge_ratio;  // node2vec: merge N(prev) when d_prev <= ratio*d_cur + 32
+    uint32_t merge_ratio;  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };

@@ -71,59 +71,139 @@ __device__ __forceinline__ uint64_t lane_base(const WalkArgs &a, const StepCtx &
 }
 
 // ---------------------------------------------------------------------------
-// ZPRS (samplers.py:188-220): logical lanes are processed in groups of 32,
-// physical lane p of group g owning logical lane j = 32g + p.  Pass 1 sums
-// lane j's strided slice in chunk order (the reference's order), the lane
-// sums are exclusive-scanned in lane order (sequentially unless EXACT), and
-// pass 2 runs lane j's reservoir.  The winner is the highest logical lane
-// holding a candidate (_kernels.py:459-462), so later groups override.
+// ZPRS (samplers.py:188-220).  Logical lane j owns elements j, j+k, j+2k...
+// and physical lane p of group g plays logical lane j = 32g + p, so each
+// lane's pass-1 sum and pass-2 running prefix accumulate in chunk order --
+// the reference's own order -- and only the exclusive scan over lanes needs
+// care (sequential unless EXACT).  The winner is the highest logical lane
+// holding a candidate (_kernels.py:459-462), so pass 2 walks the groups from
+// the top and stops at the first group with a candidate: lanes below it
+// cannot change the result (about half the RNG work saved on hub steps).
+// For deg <= kHashSlots the app weights of pass 1 are staged in the warp's
+// shared memory (exact as float for DeepWalk/PPR/MetaPath) and pass 2 reads
+// them from there instead of re-reading global memory.
 // ---------------------------------------------------------------------------
 template <int APP, bool EXACT>
-__device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane) {
+__device__ __forceinline__ double lane_excl_scan(double lsum, double &ecarry, int lane) {
+    double excl;
+    if constexpr (EXACT) {
+        const double incl = warp_incl_scan(lsum, lane);
+        const double up = __shfl_up_sync(FULL, incl, 1);
+        excl = __dadd_rn(ecarry, lane == 0 ? 0.0 : up);
+        ecarry = __dadd_rn(ecarry, __shfl_sync(FULL, incl, 31));
+    } else {  // run = 0; prefix[j] = run; run += lane_w[j]  (_kernels.py:441-444)
+        double run = ecarry;
+        excl = 0.0;
+#pragma unroll 1
+        for (int t = 0; t < 32; t++) {
+            const double lt = __shfl_sync(FULL, lsum, t);
+            if (lane == t) excl = run;
+            run = __dadd_rn(run, lt);
+        }
+        ecarry = run;
+    }
+    return excl;
+}
+
+template <int APP>
+__device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const StepCtx &s,
+                                                    uint32_t j, uint32_t k, double run,
+                                                    const float *stage) {
+    uint32_t cand = 0;
+    uint64_t word = lane_base(a, s, j);
+    const uint32_t deg = s.deg;
+    if (stage) {
+#pragma unroll 4
+        for (uint32_t i = j; i < deg; i += k, word += GOLDEN) {
+            const double wv = (double)stage[i];
+            run = __dadd_rn(run, wv);
+            const double r = u01_word(word);
+            if (wv > 0.0 && __dmul_rn(r, run) < wv) cand = i + 1;
+        }
+    } else {
+#pragma unroll 4
+        for (uint32_t i = j; i < deg; i += k, word += GOLDEN) {
+            const double wv = elem_weight<APP>(a, s, i);
+            run = __dadd_rn(run, wv);
+            const double r = u01_word(word);
+            if (wv > 0.0 && __dmul_rn(r, run) < wv) cand = i + 1;
+        }
+    }
+    return cand;
+}
+
+template <int APP, bool EXACT>
+__device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
+                              uint32_t *wsm) {
     const uint32_t deg = s.deg;
     const uint32_t nl = k < deg ? k : deg;
+    // app weights are exactly representable as float except for node2vec
+    float *stage = (APP != APP_NODE2VEC && deg <= kHashSlots)
+                       ? reinterpret_cast<float *>(wsm) : nullptr;
+    if (nl <= 32) {  // one group: physical lane == logical lane
+        const uint32_t j = lane;
+        double lsum = 0.0;
+        if (j < nl) {
+#pragma unroll 4
+            for (uint32_t i = j; i < deg; i += k) {
+                const double wv = elem_weight<APP>(a, s, i);
+                if (stage) stage[i] = (float)wv;
+                lsum = __dadd_rn(lsum, wv);
+            }
+        }
+        double ecarry = 0.0;
+        const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
+        const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, stage) : 0;
+        const unsigned m = __ballot_sync(FULL, cand > 0);
+        const uint32_t c = __shfl_sync(FULL, cand, m ? 31 - __clz(m) : 0);
+        __syncwarp();
+        return m ? c : 0;
+    }
+    if (nl <= 256) {  // up to 8 groups: lane sums -> exclusive prefixes in smem
+        double *E = reinterpret_cast<double *>(wsm + kHashSlots);
+        const uint32_t ng = (nl + 31) >> 5;
+        double ecarry = 0.0;
+        for (uint32_t g = 0; g < ng; g++) {
+            const uint32_t j = g * 32 + lane;
+            double lsum = 0.0;
+            if (j < nl) {
+#pragma unroll 4
+                for (uint32_t i = j; i < deg; i += k) {
+                    const double wv = elem_weight<APP>(a, s, i);
+                    if (stage) stage[i] = (float)wv;
+                    lsum = __dadd_rn(lsum, wv);
+                }
+            }
+            E[j] = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
+        }
+        __syncwarp();
+        uint32_t best = 0;
+        for (int g = (int)ng - 1; g >= 0; g--) {
+            const uint32_t j = g * 32 + lane;
+            const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, E[j], stage) : 0;
+            const unsigned m = __ballot_sync(FULL, cand > 0);
+            if (m) {
+                best = __shfl_sync(FULL, cand, 31 - __clz(m));
+                break;
+            }
+        }
+        __syncwarp();
+        return best;
+    }
+    // k > 256: group by group, upward (generic k, correctness path)
     double ecarry = 0.0;
     uint32_t best = 0;
     for (uint32_t g0 = 0; g0 < nl; g0 += 32) {
         const uint32_t j = g0 + lane;
-        const bool act = j < nl;
         double lsum = 0.0;
-        if (act) {
+        if (j < nl) {
 #pragma unroll 4
             for (uint32_t i = j; i < deg; i += k) lsum = __dadd_rn(lsum, elem_weight<APP>(a, s, i));
         }
-        double excl;
-        if constexpr (EXACT) {
-            const double incl = warp_incl_scan(lsum, lane);
-            double up = __shfl_up_sync(FULL, incl, 1);
-            excl = __dadd_rn(ecarry, lane == 0 ? 0.0 : up);
-            ecarry = __dadd_rn(ecarry, __shfl_sync(FULL, incl, 31));
-        } else {
-            double run = ecarry;
-            excl = 0.0;
-#pragma unroll 1
-            for (int t = 0; t < 32; t++) {
-                const double lt = __shfl_sync(FULL, lsum, t);
-                if (lane == t) excl = run;
-                run = __dadd_rn(run, lt);
-            }
-            ecarry = run;
-        }
-        uint32_t cand = 0;
-        if (act) {
-            double run = excl;
-            uint64_t word = lane_base(a, s, j);
-#pragma unroll 4
-            for (uint32_t i = j; i < deg; i += k, word += GOLDEN) {
-                const double wv = elem_weight<APP>(a, s, i);
-                run = __dadd_rn(run, wv);
-                const double r = u01_word(word);
-                if (wv > 0.0 && __dmul_rn(r, run) < wv) cand = i + 1;
-            }
-        }
+        const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
+        const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, nullptr) : 0;
         const unsigned m = __ballot_sync(FULL, cand > 0);
-        const int src = m ? 31 - __clz(m) : 0;
-        const uint32_t c = __shfl_sync(FULL, cand, src);
+        const uint32_t c = __shfl_sync(FULL, cand, m ? 31 - __clz(m) : 0);
         if (m) best = c;
     }
     return best;
@@ -214,41 +294,50 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
 // ---------------------------------------------------------------------------
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
+// Bucketed open addressing: 4 slots (16 bytes) per bucket, filled in slot
+// order, buckets probed linearly.  A lookup is one LDS.128; it continues to
+// the next bucket only when the bucket is full and the key is absent (rare
+// at load <= 1/4), so a warp rarely waits on its slowest lane.
 struct HashWin {
     const uint32_t *P;  // N(prev)
-    uint32_t *tab;      // per-warp table (kHashSlots)
+    uint4 *tab;         // per-warp buckets (kHashSlots / 4), shared memory
     uint32_t dp;        // d(prev)
     uint32_t c0, cn;    // current chunk [c0, c0+cn)
     uint32_t cmax;      // P[c0+cn-1]
-    uint32_t hshift;    // 32 - log2(table size)
-    uint32_t hmask;
+    uint32_t hshift;    // 32 - log2(#buckets)
+    uint32_t bmask;
     bool last;          // chunk reaches the end of N(prev)
 };
 
-__device__ __forceinline__ uint32_t hslot(uint32_t u, uint32_t shift) {
+__device__ __forceinline__ uint32_t hbucket(uint32_t u, uint32_t shift) {
     return (u * 0x9E3779B1u) >> shift;
 }
 
 // (Re)build the table from P[c0, c0 + min(kChunk, dp - c0)).
 __device__ __forceinline__ void hash_build(HashWin &H, int lane) {
     H.cn = min(kChunk, H.dp - H.c0);
-    uint32_t bits = 6;
-    while ((1u << bits) < 2 * H.cn) bits++;
-    const uint32_t size = 1u << bits;
+    uint32_t bits = 3;
+    while ((1u << bits) < H.cn) bits++;  // >= cn buckets: load <= 1/4
+    const uint32_t nb = 1u << bits;
     H.hshift = 32 - bits;
-    H.hmask = size - 1;
+    H.bmask = nb - 1;
     __syncwarp();
-    for (uint32_t x = lane * 4; x < size; x += 128)
-        *reinterpret_cast<uint4 *>(H.tab + x) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    for (uint32_t x = lane; x < nb; x += 32) H.tab[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncwarp();
     const uint32_t *src = H.P + H.c0;
+    uint32_t *slots = reinterpret_cast<uint32_t *>(H.tab);
     for (uint32_t x = lane; x < H.cn; x += 32) {
         const uint32_t key = ldg(src + x);
-        uint32_t sl = hslot(key, H.hshift);
+        uint32_t b = hbucket(key, H.hshift);
         for (;;) {
-            const uint32_t old = atomicCAS(H.tab + sl, kEmpty, key);
+            uint32_t old = kEmpty;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                old = atomicCAS(slots + b * 4 + q, kEmpty, key);
+                if (old == kEmpty || old == key) break;
+            }
             if (old == kEmpty || old == key) break;
-            sl = (sl + 1) & H.hmask;
+            b = (b + 1) & H.bmask;
         }
     }
     H.cmax = ldg(src + H.cn - 1);
@@ -256,37 +345,51 @@ __device__ __forceinline__ void hash_build(HashWin &H, int lane) {
     __syncwarp();
 }
 
-__device__ __forceinline__ bool hash_probe(const HashWin &H, uint32_t u) {
-    uint32_t sl = hslot(u, H.hshift);
+__device__ __forceinline__ bool bucket_has(const uint4 q, uint32_t u) {
+    return q.x == u || q.y == u || q.z == u || q.w == u;
+}
+
+// Slow tail of a lookup whose first bucket was full.
+__device__ __forceinline__ bool hash_probe_tail(const uint4 *tab, uint32_t b, uint32_t bmask,
+                                                uint32_t u) {
     for (;;) {
-        const uint32_t key = H.tab[sl];
-        if (key == u) return true;
-        if (key == kEmpty) return false;
-        sl = (sl + 1) & H.hmask;
+        b = (b + 1) & bmask;
+        const uint4 q = tab[b];
+        if (bucket_has(q, u)) return true;
+        if (q.w == kEmpty) return false;
     }
 }
 
-// Membership for the 4 elements of this lane (need[e] masks them).
-__device__ __forceinline__ void member4_hash(HashWin &H, const uint32_t u[4], bool need[4],
-                                            bool mem[4], int lane) {
+// Membership bits for this lane's 4 elements; `need` masks the lookups.
+__device__ __forceinline__ uint32_t member4_hash(HashWin &H, const uint32_t u[4], uint32_t need,
+                                                int lane) {
+    uint32_t mem = 0;
     for (;;) {
-        bool pending = false;
+        uint32_t here = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (((need >> e) & 1) && (u[e] <= H.cmax || H.last)) here |= 1u << e;
+        uint32_t full = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            if (need[e]) {
-                if (u[e] <= H.cmax || H.last) {
-                    mem[e] = hash_probe(H, u[e]);
-                    need[e] = false;
-                } else {
-                    pending = true;
-                }
+            if ((here >> e) & 1) {
+                const uint4 q = H.tab[hbucket(u[e], H.hshift)];
+                if (bucket_has(q, u[e])) mem |= 1u << e;
+                else if (q.w != kEmpty) full |= 1u << e;
             }
         }
-        if (!__any_sync(FULL, pending)) return;
+        if (full) {
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+                if (((full >> e) & 1) && hash_probe_tail(H.tab, hbucket(u[e], H.hshift), H.bmask, u[e]))
+                    mem |= 1u << e;
+        }
+        need &= ~here;
+        if (!__any_sync(FULL, need)) return mem;
         uint32_t umin = kEmpty;
 #pragma unroll
         for (int e = 3; e >= 0; e--)
-            if (need[e]) umin = u[e];
+            if ((need >> e) & 1) umin = u[e];
         umin = __reduce_min_sync(FULL, umin);
         // advance: skip whole chunks that end below every pending u
         uint32_t c0 = H.c0 + H.cn;
@@ -297,37 +400,38 @@ __device__ __forceinline__ void member4_hash(HashWin &H, const uint32_t u[4], bo
 }
 
 // 4 independent branchless binary searches over P[0, dp) (global memory).
-__device__ __forceinline__ void member4_bsearch(const uint32_t *__restrict__ P, uint32_t dp,
-                                               const uint32_t u[4], const bool need[4],
-                                               bool mem[4]) {
+__device__ __forceinline__ uint32_t member4_bsearch(const uint32_t *__restrict__ P, uint32_t dp,
+                                                   const uint32_t u[4], uint32_t need) {
     uint32_t b[4] = {0, 0, 0, 0};
     uint32_t n = dp;
     while (n > 1) {
         const uint32_t half = n >> 1;
 #pragma unroll
-        for (int e = 0; e < 4; e++)
-            b[e] = ldg(P + b[e] + half) <= u[e] ? b[e] + half : b[e];
+        for (int e = 0; e < 4; e++) b[e] = ldg(P + b[e] + half) <= u[e] ? b[e] + half : b[e];
         n -= half;
     }
+    uint32_t mem = 0;
 #pragma unroll
-    for (int e = 0; e < 4; e++) mem[e] = need[e] && dp > 0 && ldg(P + b[e]) == u[e];
+    for (int e = 0; e < 4; e++)
+        if (((need >> e) & 1) && ldg(P + b[e]) == u[e]) mem |= 1u << e;
+    return mem;
 }
 
+template <bool KPOW2>
 __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                    uint32_t *wsm, uint32_t &sel_u) {
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
     // lane bases (power-of-two k <= 256) -> shared memory
     uint64_t *sb = reinterpret_cast<uint64_t *>(wsm + kHashSlots);
-    const bool kpow2 = k <= 256 && (k & (k - 1)) == 0;
     const uint32_t kshift = 31 - __clz(k), kmask = k - 1;
-    if (kpow2) {
+    if (KPOW2) {
         const uint32_t nl = min(k, deg);
         for (uint32_t j = lane; j < nl; j += 32) sb[j] = lane_base(a, s, j);
     }
     HashWin H;
     H.P = a.tgt + s.plo;
-    H.tab = wsm;
+    H.tab = reinterpret_cast<uint4 *>(wsm);
     H.dp = (uint32_t)(s.phi - s.plo);
     const bool use_hash = H.dp <= a.merge_ratio * deg + 2 * kChunk;
     if (use_hash) {
@@ -360,19 +464,22 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         const int32_t i0 = (int32_t)(t * 128 + lane * 4) - (int32_t)off;
         const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
         const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
-        bool valid[4], need[4], mem[4] = {false, false, false, false};
+        uint32_t vmask = 0xFu;
+        if (i0 < 0) vmask &= 0xFu << (-i0);
+        const int32_t rem = (int32_t)deg - i0;
+        if (rem < 4) vmask &= rem <= 0 ? 0u : (1u << rem) - 1;
+        uint32_t pmask = 0;
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-            valid[e] = i0 + e >= 0 && i0 + e < (int32_t)deg;
-            need[e] = valid[e] && u[e] != prev;
-        }
-        if (use_hash) member4_hash(H, u, need, mem, lane);
-        else member4_bsearch(H.P, H.dp, u, need, mem);
+        for (int e = 0; e < 4; e++) pmask |= (u[e] == prev ? 1u : 0u) << e;
+        const uint32_t need = vmask & ~pmask;
+        const uint32_t mem = use_hash ? member4_hash(H, u, need, lane)
+                                      : member4_bsearch(H.P, H.dp, u, need);
         double wv[4], pre[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            const double bse = u[e] == prev ? a.inv_a : (mem[e] ? 1.0 : a.inv_b);
-            wv[e] = valid[e] ? (a.weighted ? __dmul_rn(bse, (double)wf[e]) : bse) : 0.0;
+            const double bse = ((pmask >> e) & 1) ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
+            const double x = a.weighted ? __dmul_rn(bse, (double)wf[e]) : bse;
+            wv[e] = ((vmask >> e) & 1) ? x : 0.0;
         }
         pre[0] = wv[0];
         pre[1] = __dadd_rn(pre[0], wv[1]);
@@ -383,17 +490,15 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         const double base = __dadd_rn(carry, lane == 0 ? 0.0 : excl);
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            if (wv[e] > 0.0) {
-                const uint32_t i = (uint32_t)(i0 + e);
-                uint64_t word;
-                if (kpow2) word = sb[i & kmask] + (uint64_t)(i >> kshift) * GOLDEN;
-                else word = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
-                const double r = u01_word(word);
-                const double P = __dadd_rn(base, pre[e]);
-                if (__dmul_rn(r, P) < wv[e]) {
-                    cand = i + 1;
-                    cand_u = u[e];
-                }
+            const uint32_t i = (uint32_t)(i0 + e);
+            uint64_t word;
+            if (KPOW2) word = sb[i & kmask] + (uint64_t)(i >> kshift) * GOLDEN;
+            else word = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
+            const double r = u01_word(word);
+            const double P = __dadd_rn(base, pre[e]);
+            if (wv[e] > 0.0 && __dmul_rn(r, P) < wv[e]) {
+                cand = i + 1;
+                cand_u = u[e];
             }
         }
         carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
@@ -494,7 +599,10 @@ walk_kernel(const WalkArgs a) {
             if constexpr (SAMPLER == SAMPLER_DPRS) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
-                        sel = dprs_n2v_exact(a, s, k, lane, wsm, sel_u);
+                        if (k <= 256 && (k & (k - 1)) == 0)
+                            sel = dprs_n2v_exact<true>(a, s, k, lane, wsm, sel_u);
+                        else
+                            sel = dprs_n2v_exact<false>(a, s, k, lane, wsm, sel_u);
                         have_u = true;
                     } else {
                         sel = dprs_warp_exact<APP>(a, s, k, lane);
@@ -507,7 +615,7 @@ walk_kernel(const WalkArgs a) {
                 st[ST_COLLECTIVES] += 2 * chunks;
                 st[ST_EDGES] += s.deg;
             } else {
-                sel = zprs_warp<APP, EXACT>(a, s, k, lane);
+                sel = zprs_warp<APP, EXACT>(a, s, k, lane, wsm);
                 st[ST_COLLECTIVES] += 2;
                 st[ST_EDGES] += 2 * s.deg;
             }

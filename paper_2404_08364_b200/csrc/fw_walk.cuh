@@ -11,7 +11,7 @@ constexpr int kWalkThreads = 256;  // 8 warp walkers per CTA
 constexpr int kWalkMinBlocks = FW_MIN_BLOCKS;  // >= 32 resident warps per SM
 // per-warp shared memory: N(prev) hash window + 256 staged lane bases
 constexpr uint32_t kHashSlots = 1024;
-constexpr uint32_t kChunk = 512;  // N(prev) entries hashed at a time (load <= 1/2)
+constexpr uint32_t kChunk = 256;  // N(prev) entries hashed at a time (load <= 1/4)
 constexpr uint32_t kWarpSmemWords = kHashSlots + 2 * 256;
 constexpr int kWalkSmemBytes = (kWalkThreads / 32) * kWarpSmemWords * 4;
 

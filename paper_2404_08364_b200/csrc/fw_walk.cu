@@ -22,6 +22,9 @@
 
 namespace fw {
 
+// Dynamic shared memory: kWarpSmemWords words per warp (see fw_walk.cuh).
+extern __shared__ __align__(16) uint32_t fw_smem[];
+
 struct StepCtx {
     int64_t elo;      // offsets[cur]
     uint32_t deg;     // offsets[cur+1] - offsets[cur] (host checks d_max < 2^32)
@@ -294,13 +297,35 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
 // ---------------------------------------------------------------------------
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
-// Bucketed open addressing: 4 slots (16 bytes) per bucket, filled in slot
-// order, buckets probed linearly.  A lookup is one LDS.128; it continues to
-// the next bucket only when the bucket is full and the key is absent (rare
-// at load <= 1/4), so a warp rarely waits on its slowest lane.
+// fp64 shuffles as two explicit 32-bit shuffles (the 64-bit overloads
+// compile to extra register swaps on this toolchain).
+__device__ __forceinline__ double shfl_up_d(double x, int d) {
+    const int lo = __shfl_up_sync(FULL, __double2loint(x), d);
+    const int hi = __shfl_up_sync(FULL, __double2hiint(x), d);
+    return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ double shfl_d(double x, int src) {
+    const int lo = __shfl_sync(FULL, __double2loint(x), src);
+    const int hi = __shfl_sync(FULL, __double2hiint(x), src);
+    return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double o = shfl_up_d(v, d);
+        if (lane >= d) v = __dadd_rn(v, o);
+    }
+    return v;
+}
+
+// Bucketed open addressing in the warp's shared-memory slice: 4 slots (16
+// bytes) per bucket, filled in slot order, buckets probed linearly.  A
+// lookup is one LDS.128; it continues to the next bucket only when the
+// bucket is full and the key is absent (rare at load <= 1/4), so a warp
+// rarely waits on its slowest lane.
 struct HashWin {
     const uint32_t *P;  // N(prev)
-    uint4 *tab;         // per-warp buckets (kHashSlots / 4), shared memory
+    uint32_t tab;       // word offset of the table in fw_smem
     uint32_t dp;        // d(prev)
     uint32_t c0, cn;    // current chunk [c0, c0+cn)
     uint32_t cmax;      // P[c0+cn-1]
@@ -312,6 +337,9 @@ struct HashWin {
 __device__ __forceinline__ uint32_t hbucket(uint32_t u, uint32_t shift) {
     return (u * 0x9E3779B1u) >> shift;
 }
+__device__ __forceinline__ uint4 bucket_at(uint32_t tab, uint32_t b) {
+    return reinterpret_cast<const uint4 *>(fw_smem + tab)[b];
+}
 
 // (Re)build the table from P[c0, c0 + min(kChunk, dp - c0)).
 __device__ __forceinline__ void hash_build(HashWin &H, int lane) {
@@ -322,10 +350,10 @@ __device__ __forceinline__ void hash_build(HashWin &H, int lane) {
     H.hshift = 32 - bits;
     H.bmask = nb - 1;
     __syncwarp();
-    for (uint32_t x = lane; x < nb; x += 32) H.tab[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + H.tab);
+    for (uint32_t x = lane; x < nb; x += 32) t4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncwarp();
     const uint32_t *src = H.P + H.c0;
-    uint32_t *slots = reinterpret_cast<uint32_t *>(H.tab);
     for (uint32_t x = lane; x < H.cn; x += 32) {
         const uint32_t key = ldg(src + x);
         uint32_t b = hbucket(key, H.hshift);
@@ -333,7 +361,7 @@ __device__ __forceinline__ void hash_build(HashWin &H, int lane) {
             uint32_t old = kEmpty;
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                old = atomicCAS(slots + b * 4 + q, kEmpty, key);
+                old = atomicCAS(fw_smem + H.tab + b * 4 + q, kEmpty, key);
                 if (old == kEmpty || old == key) break;
             }
             if (old == kEmpty || old == key) break;
@@ -350,11 +378,11 @@ __device__ __forceinline__ bool bucket_has(const uint4 q, uint32_t u) {
 }
 
 // Slow tail of a lookup whose first bucket was full.
-__device__ __forceinline__ bool hash_probe_tail(const uint4 *tab, uint32_t b, uint32_t bmask,
+__device__ __forceinline__ bool hash_probe_tail(uint32_t tab, uint32_t b, uint32_t bmask,
                                                 uint32_t u) {
     for (;;) {
         b = (b + 1) & bmask;
-        const uint4 q = tab[b];
+        const uint4 q = bucket_at(tab, b);
         if (bucket_has(q, u)) return true;
         if (q.w == kEmpty) return false;
     }
@@ -365,15 +393,12 @@ __device__ __forceinline__ uint32_t member4_hash(HashWin &H, const uint32_t u[4]
                                                 int lane) {
     uint32_t mem = 0;
     for (;;) {
-        uint32_t here = 0;
-#pragma unroll
-        for (int e = 0; e < 4; e++)
-            if (((need >> e) & 1) && (u[e] <= H.cmax || H.last)) here |= 1u << e;
-        uint32_t full = 0;
+        uint32_t here = 0, full = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            if ((here >> e) & 1) {
-                const uint4 q = H.tab[hbucket(u[e], H.hshift)];
+            if (((need >> e) & 1) && (u[e] <= H.cmax || H.last)) {
+                here |= 1u << e;
+                const uint4 q = bucket_at(H.tab, hbucket(u[e], H.hshift));
                 if (bucket_has(q, u[e])) mem |= 1u << e;
                 else if (q.w != kEmpty) full |= 1u << e;
             }
@@ -381,7 +406,8 @@ __device__ __forceinline__ uint32_t member4_hash(HashWin &H, const uint32_t u[4]
         if (full) {
 #pragma unroll
             for (int e = 0; e < 4; e++)
-                if (((full >> e) & 1) && hash_probe_tail(H.tab, hbucket(u[e], H.hshift), H.bmask, u[e]))
+                if (((full >> e) & 1) &&
+                    hash_probe_tail(H.tab, hbucket(u[e], H.hshift), H.bmask, u[e]))
                     mem |= 1u << e;
         }
         need &= ~here;
@@ -417,39 +443,56 @@ __device__ __forceinline__ uint32_t member4_bsearch(const uint32_t *__restrict__
     return mem;
 }
 
-template <bool KPOW2>
+// KMODE 1: k == 32 (lane bases of this lane's 4 slots live in registers:
+//          slot e always maps to logical lane (4p+e-off) mod 32, its counter
+//          advances by 4 per 128-element tile);
+// KMODE 2: power-of-two 4 <= k <= 256, bases staged in shared memory with a
+//          bank-conflict-free layout (j & 3) * k/4 + j/4;
+// KMODE 0: any other k (bases recomputed per element).
+template <int KMODE>
 __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
-                                   uint32_t *wsm, uint32_t &sel_u) {
+                                   uint32_t woff, uint32_t &sel_u) {
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
-    // lane bases (power-of-two k <= 256) -> shared memory
-    uint64_t *sb = reinterpret_cast<uint64_t *>(wsm + kHashSlots);
-    const uint32_t kshift = 31 - __clz(k), kmask = k - 1;
-    if (KPOW2) {
+    const uint32_t off = (uint32_t)(s.elo & 3);
+    const uint32_t kq = k >> 2;            // KMODE 2: bases per row
+    const uint32_t kshift = 31 - __clz(k);  // log2 k for powers of two
+    const uint32_t sbw = woff + kHashSlots;  // word offset of the staged bases
+    uint64_t word[4];
+    if constexpr (KMODE == 1) {
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const int32_t i = lane * 4 + e - (int32_t)off;
+            word[e] = lane_base(a, s, (uint32_t)i & 31u) + (uint64_t)(int64_t)(i >> 5) * GOLDEN;
+        }
+    }
+    if constexpr (KMODE == 2) {
         const uint32_t nl = min(k, deg);
-        for (uint32_t j = lane; j < nl; j += 32) sb[j] = lane_base(a, s, j);
+        uint64_t *sb = reinterpret_cast<uint64_t *>(fw_smem + sbw);
+        for (uint32_t j = lane; j < nl; j += 32) sb[(j & 3) * kq + (j >> 2)] = lane_base(a, s, j);
     }
     HashWin H;
     H.P = a.tgt + s.plo;
-    H.tab = reinterpret_cast<uint4 *>(wsm);
+    H.tab = woff;
     H.dp = (uint32_t)(s.phi - s.plo);
     const bool use_hash = H.dp <= a.merge_ratio * deg + 2 * kChunk;
     if (use_hash) {
         H.c0 = 0;
-        hash_build(H, lane);  // (ends with __syncwarp: sb[] visible too)
+        hash_build(H, lane);  // (ends with __syncwarp: staged bases visible too)
     } else {
         __syncwarp();
     }
-    const uint32_t off = (uint32_t)(s.elo & 3);
     const uint32_t span = deg + off;
     const uint32_t ntiles = (span + 127) >> 7;
     const uint4 *T4 = reinterpret_cast<const uint4 *>(a.tgt + (s.elo - off));
     const float4 *W4 = reinterpret_cast<const float4 *>(a.w + (s.elo - off));
+    const bool weighted = a.weighted != 0;
+    const double inv_a = a.inv_a, inv_b = a.inv_b;
     uint4 nu = make_uint4(0, 0, 0, 0);
     float4 nw = make_float4(1.f, 1.f, 1.f, 1.f);
     if ((uint32_t)lane * 4 < span) {
         nu = ldg(T4 + lane);
-        if (a.weighted) nw = ldg(W4 + lane);
+        if (weighted) nw = ldg(W4 + lane);
     }
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
@@ -459,7 +502,7 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         const uint32_t nx = (t + 1) * 128 + lane * 4;
         if (nx < span) {  // prefetch the next tile
             nu = ldg(T4 + (nx >> 2));
-            if (a.weighted) nw = ldg(W4 + (nx >> 2));
+            if (weighted) nw = ldg(W4 + (nx >> 2));
         }
         const int32_t i0 = (int32_t)(t * 128 + lane * 4) - (int32_t)off;
         const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
@@ -474,34 +517,43 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         const uint32_t need = vmask & ~pmask;
         const uint32_t mem = use_hash ? member4_hash(H, u, need, lane)
                                       : member4_bsearch(H.P, H.dp, u, need);
-        double wv[4], pre[4];
+        double wv[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            const double bse = ((pmask >> e) & 1) ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
-            const double x = a.weighted ? __dmul_rn(bse, (double)wf[e]) : bse;
+            const double bse = ((pmask >> e) & 1) ? inv_a : (((mem >> e) & 1) ? 1.0 : inv_b);
+            const double x = weighted ? __dmul_rn(bse, (double)wf[e]) : bse;
             wv[e] = ((vmask >> e) & 1) ? x : 0.0;
         }
-        pre[0] = wv[0];
-        pre[1] = __dadd_rn(pre[0], wv[1]);
-        pre[2] = __dadd_rn(pre[1], wv[2]);
-        pre[3] = __dadd_rn(pre[2], wv[3]);
-        const double incl = warp_incl_scan(pre[3], lane);
-        const double excl = __shfl_up_sync(FULL, incl, 1);
-        const double base = __dadd_rn(carry, lane == 0 ? 0.0 : excl);
+        const double p1 = __dadd_rn(wv[0], wv[1]);
+        const double p2 = __dadd_rn(p1, wv[2]);
+        const double p3 = __dadd_rn(p2, wv[3]);
+        const double incl = warp_incl_scan_d(p3, lane);
+        const double excl = __dadd_rn(incl, -p3);  // exact (EXACT mode)
+        const double base = __dadd_rn(carry, excl);
+        const double pre[4] = {wv[0], p1, p2, p3};
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const uint32_t i = (uint32_t)(i0 + e);
-            uint64_t word;
-            if (KPOW2) word = sb[i & kmask] + (uint64_t)(i >> kshift) * GOLDEN;
-            else word = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
-            const double r = u01_word(word);
+            uint64_t wd;
+            if constexpr (KMODE == 1) {
+                wd = word[e];
+                word[e] += 4 * GOLDEN;
+            } else if constexpr (KMODE == 2) {
+                const uint32_t j = i & (k - 1);
+                const uint64_t b = reinterpret_cast<const uint64_t *>(fw_smem + sbw)
+                    [((uint32_t)(e - (int)off) & 3u) * kq + (j >> 2)];
+                wd = b + (uint64_t)(i >> kshift) * GOLDEN;
+            } else {
+                wd = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
+            }
+            const double r = u01_word(wd);
             const double P = __dadd_rn(base, pre[e]);
             if (wv[e] > 0.0 && __dmul_rn(r, P) < wv[e]) {
                 cand = i + 1;
                 cand_u = u[e];
             }
         }
-        carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
+        carry = __dadd_rn(carry, shfl_d(incl, 31));
     }
     const uint32_t sel = __reduce_max_sync(FULL, cand);
     const unsigned who = __ballot_sync(FULL, cand == sel);
@@ -538,6 +590,10 @@ __device__ uint32_t dprs_warp_ordered(const WalkArgs &a, const StepCtx &s, uint3
     return __reduce_max_sync(FULL, cand);
 }
 
+__device__ __forceinline__ void stat_add(unsigned long long *st, int idx, long long v, int lane) {
+    if (lane == 0) st[idx] += (unsigned long long)v;
+}
+
 // ---------------------------------------------------------------------------
 // The persistent walker.
 // ---------------------------------------------------------------------------
@@ -545,11 +601,14 @@ template <int APP, int SAMPLER, bool EXACT>
 __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks)
 walk_kernel(const WalkArgs a) {
     const int lane = threadIdx.x & 31;
-    extern __shared__ __align__(16) uint32_t fw_smem[];
-    uint32_t *wsm = fw_smem + (threadIdx.x >> 5) * kWarpSmemWords;
-    long long st[ST_COUNT];
-#pragma unroll
-    for (int i = 0; i < ST_COUNT; i++) st[i] = 0;
+    const uint32_t woff = (threadIdx.x >> 5) * kWarpSmemWords;
+    uint32_t *wsm = fw_smem + woff;
+    // per-warp RunStats counters live in shared memory (registers are the
+    // scarce resource in the sampler loops); every lane keeps the same value
+    // in flight, lane 0 owns the slot.
+    unsigned long long *st = reinterpret_cast<unsigned long long *>(fw_smem + woff + kStatsWord);
+    if (lane < ST_COUNT) st[lane] = 0;
+    __syncwarp();
 
     for (;;) {
         unsigned long long qi = 0;
@@ -569,15 +628,15 @@ walk_kernel(const WalkArgs a) {
             s.deg = (uint32_t)(ldg(a.off + cur + 1) - s.elo);
             const bool small = (int64_t)s.deg <= a.d_t;
             const uint32_t k = (uint32_t)(small ? a.k_small : a.k_big);
-            st[ST_SMALL] += small ? 1 : 0;
-            st[ST_LARGE] += small ? 0 : 1;
-            st[ST_STEPS] += 1;
-            st[ST_BYTES] += 16;
+            stat_add(st, ST_SMALL, small ? 1 : 0, lane);
+            stat_add(st, ST_LARGE, small ? 0 : 1, lane);
+            stat_add(st, ST_STEPS, 1, lane);
+            stat_add(st, ST_BYTES, 16, lane);
             const uint64_t step = emitted;
             s.A = (TAG_REPLAY | (q << 30) | (step << 10)) * MIX1;
             if constexpr (APP == APP_PPR) {
                 const double r = u01(mix64(a.h ^ (s.A + STOP_LANE * MIX1)), 0);
-                st[ST_DRAWS] += 1;
+                stat_add(st, ST_DRAWS, 1, lane);
                 if (r < a.stop_prob) break;
             }
             if (s.deg == 0) break;
@@ -589,7 +648,7 @@ walk_kernel(const WalkArgs a) {
                 if (s.prev >= 0) {  // N(prev) = the previous step's N(cur)
                     s.plo = pelo;
                     s.phi = pelo + pdeg;
-                    st[ST_BYTES] += 16 + 4 * pdeg;
+                    stat_add(st, ST_BYTES, 16 + 4 * pdeg, lane);
                 }
             }
             const uint32_t chunks = (s.deg - 1) / k + 1;
@@ -599,10 +658,10 @@ walk_kernel(const WalkArgs a) {
             if constexpr (SAMPLER == SAMPLER_DPRS) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
-                        if (k <= 256 && (k & (k - 1)) == 0)
-                            sel = dprs_n2v_exact<true>(a, s, k, lane, wsm, sel_u);
+                        if (k >= 4 && k <= 256 && (k & (k - 1)) == 0)
+                            sel = dprs_n2v_exact<2>(a, s, k, lane, woff, sel_u);
                         else
-                            sel = dprs_n2v_exact<false>(a, s, k, lane, wsm, sel_u);
+                            sel = dprs_n2v_exact<0>(a, s, k, lane, woff, sel_u);
                         have_u = true;
                     } else {
                         sel = dprs_warp_exact<APP>(a, s, k, lane);
@@ -612,20 +671,20 @@ walk_kernel(const WalkArgs a) {
                 } else {
                     sel = dprs_warp_ordered<APP>(a, s, k, lane);
                 }
-                st[ST_COLLECTIVES] += 2 * chunks;
-                st[ST_EDGES] += s.deg;
+                stat_add(st, ST_COLLECTIVES, 2 * chunks, lane);
+                stat_add(st, ST_EDGES, s.deg, lane);
             } else {
                 sel = zprs_warp<APP, EXACT>(a, s, k, lane, wsm);
-                st[ST_COLLECTIVES] += 2;
-                st[ST_EDGES] += 2 * s.deg;
+                stat_add(st, ST_COLLECTIVES, 2, lane);
+                stat_add(st, ST_EDGES, 2 * s.deg, lane);
             }
-            st[ST_DRAWS] += (long long)chunks * k;
-            st[ST_BYTES] += (APP == APP_METAPATH ? 9 : 8) * s.deg;
+            stat_add(st, ST_DRAWS, (long long)chunks * k, lane);
+            stat_add(st, ST_BYTES, (APP == APP_METAPATH ? 9 : 8) * s.deg, lane);
             if (sel == 0) break;
             const uint32_t u = have_u ? sel_u : ldg(a.tgt + s.elo + sel - 1);
             if (lane == (int)(step & 31)) pathbuf = u;
             emitted = (uint32_t)step + 1;
-            st[ST_BYTES] += 4;
+            stat_add(st, ST_BYTES, 4, lane);
             s.prev = cur;
             pdeg = s.deg;
             pelo = s.elo;
@@ -645,17 +704,23 @@ walk_kernel(const WalkArgs a) {
             pathbuf = 0xFFFFFFFFu;
         }
         if (lane == 0) a.out_len[qi] = emitted;
-        st[ST_SAMPLED] += emitted;
+        stat_add(st, ST_SAMPLED, emitted, lane);
     }
     if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < ST_COUNT; i++)
-            if (st[i]) atomicAdd((unsigned long long *)(a.stats + i), (unsigned long long)st[i]);
+            if (st[i]) atomicAdd((unsigned long long *)(a.stats + i), st[i]);
     }
 }
 
 template <int APP, int SAMPLER, bool EXACT>
 static cudaError_t launch_t(const WalkArgs &a, int grid, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, EXACT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmemBytes);
+        attr = true;
+    }
     walk_kernel<APP, SAMPLER, EXACT><<<grid, kWalkThreads, kWalkSmemBytes, stream>>>(a);
     return cudaGetLastError();
 }
@@ -663,6 +728,8 @@ static cudaError_t launch_t(const WalkArgs &a, int grid, cudaStream_t stream) {
 template <int APP, int SAMPLER, bool EXACT>
 static int occupancy_t() {
     int nb = 0;
+    cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, EXACT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmemBytes);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_kernel<APP, SAMPLER, EXACT>,
                                                   kWalkThreads, kWalkSmemBytes);
     return nb;

@@ -12,7 +12,8 @@ constexpr int kWalkMinBlocks = FW_MIN_BLOCKS;  // >= 32 resident warps per SM
 // per-warp shared memory: N(prev) hash window + 256 staged lane bases
 constexpr uint32_t kHashSlots = 1024;
 constexpr uint32_t kChunk = 256;  // N(prev) entries hashed at a time (load <= 1/4)
-constexpr uint32_t kWarpSmemWords = kHashSlots + 2 * 256;
+constexpr uint32_t kStatsWord = kHashSlots + 2 * 256;    // 8 x u64 RunStats counters
+constexpr uint32_t kWarpSmemWords = kStatsWord + 2 * 8;
 constexpr int kWalkSmemBytes = (kWalkThreads / 32) * kWarpSmemWords * 4;
 
 // Kernel arguments (passed by value through the constant bank).

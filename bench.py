@@ -54,7 +54,12 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--nq", type=int, default=0, help="queries per GPU (0 = one per vertex)")
+    p.add_argument("--nq", type=int, default=0, help="queries (0 = one per vertex)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="weak: every GPU walks its own full query set (disjoint global qids); "
+                        "strong: one query set partitioned over the GPUs")
+    p.add_argument("--gather", action="store_true",
+                   help="after timing, gather path segments to rank 0 (timed separately)")
     return p.parse_args()
 
 
@@ -281,29 +286,34 @@ def bench_ours(args):
     labels = args.app == "metapath"
 
     # graph: generated on rank 0, replicated over NCCL (off the timed path)
+    from paper_2404_08364_b200 import dist as fwd
+    V = 1 << args.scale
+    E_ = 16 * V
     if rank == 0:
         dg = rmat.rmat_graph_device(args.scale, labels=labels, device=local)
         arrs = [dg.offsets, dg.targets, dg.weights] + ([dg.labels] if labels else [])
-    V = 1 << args.scale
-    E_ = 16 * V
     if world > 1:
-        if rank != 0:
-            arrs = [torch.empty(V + 1, dtype=torch.int64, device=dev),
-                    torch.empty(E_, dtype=torch.int32, device=dev),
-                    torch.empty(E_, dtype=torch.float32, device=dev)]
-            if labels:
-                arrs.append(torch.empty(E_, dtype=torch.uint8, device=dev))
-        for t in arrs:
-            dist.broadcast(t, src=0)
+        sd = [(V + 1, torch.int64), (E_, torch.int32), (E_, torch.float32)] + \
+            ([(E_, torch.uint8)] if labels else [])
         torch.cuda.synchronize()
+        t_rep = time.perf_counter()
+        arrs = fwd.replicate_csr(arrs if rank == 0 else None, sd, src=0, device=dev)
+        torch.cuda.synchronize()
+        t_rep = time.perf_counter() - t_rep
         if rank != 0:
             dg = DeviceGraph(V, E_, *arrs[:3], arrs[3] if labels else None, device=local)
     handle = dg.handle(local).ptr
     hub = dg.max_degree_vertex()
-    n = args.nq if args.nq else V
-    base_qid = rank * n
-    starts_h = make_starts(args, V, hub)[:n]
-    starts = torch.from_numpy(starts_h).to(dev)
+    n_total = args.nq if args.nq else V
+    if args.scaling == "strong":
+        lo, hi = fwd.partition(n_total, world, rank)
+    else:
+        lo, hi = rank * n_total, (rank + 1) * n_total
+    n = hi - lo
+    base_qid = lo
+    starts_h = (make_starts(args, V, hub)[np.arange(lo, hi) % V] if args.scaling == "strong"
+                else make_starts(args, V, hub)[:n])
+    starts = torch.from_numpy(np.ascontiguousarray(starts_h)).to(dev)
     L = app.length
     seq = torch.empty(n * L, dtype=torch.int32, device=dev)
     lens = torch.empty(n, dtype=torch.int32, device=dev)
@@ -336,6 +346,13 @@ def bench_ours(args):
     if world > 1:
         dist.barrier()
     launch_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    gather_ms = None
+    if world > 1 and args.gather and args.scaling == "strong":
+        torch.cuda.synchronize()
+        t_g = time.perf_counter()
+        fwd.gather_paths(seq, lens, n_total, L, dst=0)
+        torch.cuda.synchronize()
+        gather_ms = 1000 * (time.perf_counter() - t_g)
     my_ms = sum(launch_ms)
     st = stats.cpu().numpy()
     sampled = int(st[6])
@@ -401,10 +418,12 @@ def bench_ours(args):
         line = {
             "metric": metric_name(args), "value": value, "unit": "steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "fp64+u64", "data": "synthetic",
             "config": {"workload": workload, "graph": f"rmat-s{args.scale}-ef16",
                        "vertices": V, "csr_entries": E_, "queries_per_gpu": n,
+                       "replicate_s": None if world == 1 else round(t_rep, 3),
+                       "gather_ms": gather_ms,
                        "parallelism": f"replicated graph, qids partitioned x{world}",
                        "l2": "inputs larger than L2 (graph + result pool > 126 MB), no flush",
                        "sampled_steps_per_gpu_step": sampled // args.steps,

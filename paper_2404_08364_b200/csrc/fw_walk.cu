@@ -22,6 +22,14 @@
 
 namespace fw {
 
+// Cold helpers (window advance, hash build, binary-search fallback): kept
+// out of line by default so their registers do not burden the tile loop.
+#ifdef FW_COLD_INLINE
+#define FW_COLD __forceinline__
+#else
+#define FW_COLD __noinline__
+#endif
+
 // Dynamic shared memory: kWarpSmemWords words per warp (see fw_walk.cuh).
 extern __shared__ __align__(16) uint32_t fw_smem[];
 
@@ -111,11 +119,12 @@ __device__ __forceinline__ double lane_excl_scan(double lsum, double &ecarry, in
 template <int APP>
 __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const StepCtx &s,
                                                     uint32_t j, uint32_t k, double run,
-                                                    const float *stage) {
+                                                    bool staged, uint32_t woff) {
+    const float *stage = reinterpret_cast<const float *>(fw_smem) + woff;
     uint32_t cand = 0;
     uint64_t word = lane_base(a, s, j);
     const uint32_t deg = s.deg;
-    if (stage) {
+    if (staged) {
 #pragma unroll 4
         for (uint32_t i = j; i < deg; i += k, word += GOLDEN) {
             const double wv = (double)stage[i];
@@ -137,12 +146,12 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
 
 template <int APP, bool EXACT>
 __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
-                              uint32_t *wsm) {
+                              uint32_t woff) {
     const uint32_t deg = s.deg;
     const uint32_t nl = k < deg ? k : deg;
     // app weights are exactly representable as float except for node2vec
-    float *stage = (APP != APP_NODE2VEC && deg <= kHashSlots)
-                       ? reinterpret_cast<float *>(wsm) : nullptr;
+    const bool staged = APP != APP_NODE2VEC && deg <= kHashSlots;
+    float *stage = reinterpret_cast<float *>(fw_smem) + woff;
     if (nl <= 32) {  // one group: physical lane == logical lane
         const uint32_t j = lane;
         double lsum = 0.0;
@@ -150,20 +159,20 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
 #pragma unroll 4
             for (uint32_t i = j; i < deg; i += k) {
                 const double wv = elem_weight<APP>(a, s, i);
-                if (stage) stage[i] = (float)wv;
+                if (staged) stage[i] = (float)wv;
                 lsum = __dadd_rn(lsum, wv);
             }
         }
         double ecarry = 0.0;
         const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
-        const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, stage) : 0;
+        const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, staged, woff) : 0;
         const unsigned m = __ballot_sync(FULL, cand > 0);
         const uint32_t c = __shfl_sync(FULL, cand, m ? 31 - __clz(m) : 0);
         __syncwarp();
         return m ? c : 0;
     }
     if (nl <= 256) {  // up to 8 groups: lane sums -> exclusive prefixes in smem
-        double *E = reinterpret_cast<double *>(wsm + kHashSlots);
+        double *E = reinterpret_cast<double *>(fw_smem + woff + kHashSlots);
         const uint32_t ng = (nl + 31) >> 5;
         double ecarry = 0.0;
         for (uint32_t g = 0; g < ng; g++) {
@@ -173,7 +182,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
 #pragma unroll 4
                 for (uint32_t i = j; i < deg; i += k) {
                     const double wv = elem_weight<APP>(a, s, i);
-                    if (stage) stage[i] = (float)wv;
+                    if (staged) stage[i] = (float)wv;
                     lsum = __dadd_rn(lsum, wv);
                 }
             }
@@ -183,7 +192,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
         uint32_t best = 0;
         for (int g = (int)ng - 1; g >= 0; g--) {
             const uint32_t j = g * 32 + lane;
-            const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, E[j], stage) : 0;
+            const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, E[j], staged, woff) : 0;
             const unsigned m = __ballot_sync(FULL, cand > 0);
             if (m) {
                 best = __shfl_sync(FULL, cand, 31 - __clz(m));
@@ -204,7 +213,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
             for (uint32_t i = j; i < deg; i += k) lsum = __dadd_rn(lsum, elem_weight<APP>(a, s, i));
         }
         const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
-        const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, nullptr) : 0;
+        const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, false, woff) : 0;
         const unsigned m = __ballot_sync(FULL, cand > 0);
         const uint32_t c = __shfl_sync(FULL, cand, m ? 31 - __clz(m) : 0);
         if (m) best = c;
@@ -322,112 +331,122 @@ __device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
 // bytes) per bucket, filled in slot order, buckets probed linearly.  A
 // lookup is one LDS.128; it continues to the next bucket only when the
 // bucket is full and the key is absent (rare at load <= 1/4), so a warp
-// rarely waits on its slowest lane.
-struct HashWin {
-    const uint32_t *P;  // N(prev)
-    uint32_t tab;       // word offset of the table in fw_smem
-    uint32_t dp;        // d(prev)
-    uint32_t c0, cn;    // current chunk [c0, c0+cn)
-    uint32_t cmax;      // P[c0+cn-1]
-    uint32_t hshift;    // 32 - log2(#buckets)
-    uint32_t bmask;
-    bool last;          // chunk reaches the end of N(prev)
-};
-
+// rarely waits on its slowest lane.  The window over N(prev) is described
+// by two registers in the hot loop (lim = max key of the chunk, or ~0 for
+// the last chunk; hshift = 32 - log2 #buckets); the rest (chunk start and
+// length, d(prev)) sits in the warp's control words (kCtlWord).
 __device__ __forceinline__ uint32_t hbucket(uint32_t u, uint32_t shift) {
     return (u * 0x9E3779B1u) >> shift;
 }
-__device__ __forceinline__ uint4 bucket_at(uint32_t tab, uint32_t b) {
-    return reinterpret_cast<const uint4 *>(fw_smem + tab)[b];
+__device__ __forceinline__ uint4 bucket_at(uint32_t woff, uint32_t b) {
+    return reinterpret_cast<const uint4 *>(fw_smem + woff)[b];
 }
-
-// (Re)build the table from P[c0, c0 + min(kChunk, dp - c0)).
-__device__ __forceinline__ void hash_build(HashWin &H, int lane) {
-    H.cn = min(kChunk, H.dp - H.c0);
-    uint32_t bits = 3;
-    while ((1u << bits) < H.cn) bits++;  // >= cn buckets: load <= 1/4
-    const uint32_t nb = 1u << bits;
-    H.hshift = 32 - bits;
-    H.bmask = nb - 1;
-    __syncwarp();
-    uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + H.tab);
-    for (uint32_t x = lane; x < nb; x += 32) t4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    __syncwarp();
-    const uint32_t *src = H.P + H.c0;
-    for (uint32_t x = lane; x < H.cn; x += 32) {
-        const uint32_t key = ldg(src + x);
-        uint32_t b = hbucket(key, H.hshift);
-        for (;;) {
-            uint32_t old = kEmpty;
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                old = atomicCAS(fw_smem + H.tab + b * 4 + q, kEmpty, key);
-                if (old == kEmpty || old == key) break;
-            }
-            if (old == kEmpty || old == key) break;
-            b = (b + 1) & H.bmask;
-        }
-    }
-    H.cmax = ldg(src + H.cn - 1);
-    H.last = H.c0 + H.cn >= H.dp;
-    __syncwarp();
-}
-
 __device__ __forceinline__ bool bucket_has(const uint4 q, uint32_t u) {
     return q.x == u || q.y == u || q.z == u || q.w == u;
 }
 
-// Slow tail of a lookup whose first bucket was full.
-__device__ __forceinline__ bool hash_probe_tail(uint32_t tab, uint32_t b, uint32_t bmask,
-                                                uint32_t u) {
-    for (;;) {
-        b = (b + 1) & bmask;
-        const uint4 q = bucket_at(tab, b);
-        if (bucket_has(q, u)) return true;
-        if (q.w == kEmpty) return false;
+// Build the table from P[c0, c0 + min(kChunk, dp - c0)); returns hshift
+// and sets lim.  Control words: [0] = c0, [1] = cn, [2] = dp.
+struct HashState {
+    uint32_t hshift, lim;
+};
+
+__device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t c0,
+                                             uint32_t dp, uint32_t woff, int lane) {
+    const uint32_t cn = min(kChunk, dp - c0);
+    uint32_t bits = 3;
+    while ((1u << bits) < cn) bits++;  // >= cn buckets: load <= 1/4
+    const uint32_t nb = 1u << bits;
+    const uint32_t shift = 32 - bits;
+    __syncwarp();
+    uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + woff);
+    for (uint32_t x = lane; x < nb; x += 32) t4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    if (lane == 0) {
+        fw_smem[woff + kCtlWord + 0] = c0;
+        fw_smem[woff + kCtlWord + 1] = cn;
+        fw_smem[woff + kCtlWord + 2] = dp;
     }
+    __syncwarp();
+    const uint32_t *src = P + c0;
+    for (uint32_t x = lane; x < cn; x += 32) {
+        const uint32_t key = ldg(src + x);
+        uint32_t b = hbucket(key, shift);
+        for (;;) {
+            uint32_t old = kEmpty;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                old = atomicCAS(fw_smem + woff + b * 4 + q, kEmpty, key);
+                if (old == kEmpty || old == key) break;
+            }
+            if (old == kEmpty || old == key) break;
+            b = (b + 1) & (nb - 1);
+        }
+    }
+    HashState hs;
+    hs.lim = c0 + cn >= dp ? kEmpty : ldg(src + cn - 1);
+    hs.hshift = shift;
+    __syncwarp();
+    return hs;
 }
 
-// Membership bits for this lane's 4 elements; `need` masks the lookups.
-__device__ __forceinline__ uint32_t member4_hash(HashWin &H, const uint32_t u[4], uint32_t need,
-                                                int lane) {
+// Lookups whose first bucket was full, and the window advance (cold path).
+struct SlowRet {
+    uint32_t mem, hshift, lim;
+};
+
+__device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ P, uint32_t woff,
+                                             uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3,
+                                             uint32_t full, uint32_t need, uint32_t hshift,
+                                             uint32_t lim, int lane) {
+    const uint32_t u[4] = {u0, u1, u2, u3};
     uint32_t mem = 0;
     for (;;) {
-        uint32_t here = 0, full = 0;
+        const uint32_t bmask = (1u << (32 - hshift)) - 1;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            if (((need >> e) & 1) && (u[e] <= H.cmax || H.last)) {
-                here |= 1u << e;
-                const uint4 q = bucket_at(H.tab, hbucket(u[e], H.hshift));
-                if (bucket_has(q, u[e])) mem |= 1u << e;
-                else if (q.w != kEmpty) full |= 1u << e;
+            if ((full >> e) & 1) {
+                uint32_t b = hbucket(u[e], hshift);
+                for (;;) {
+                    b = (b + 1) & bmask;
+                    const uint4 q = bucket_at(woff, b);
+                    if (bucket_has(q, u[e])) { mem |= 1u << e; break; }
+                    if (q.w == kEmpty) break;
+                }
             }
         }
-        if (full) {
-#pragma unroll
-            for (int e = 0; e < 4; e++)
-                if (((full >> e) & 1) &&
-                    hash_probe_tail(H.tab, hbucket(u[e], H.hshift), H.bmask, u[e]))
-                    mem |= 1u << e;
-        }
-        need &= ~here;
-        if (!__any_sync(FULL, need)) return mem;
+        if (!__any_sync(FULL, need)) return SlowRet{mem, hshift, lim};
         uint32_t umin = kEmpty;
 #pragma unroll
         for (int e = 3; e >= 0; e--)
             if ((need >> e) & 1) umin = u[e];
         umin = __reduce_min_sync(FULL, umin);
         // advance: skip whole chunks that end below every pending u
-        uint32_t c0 = H.c0 + H.cn;
-        while (c0 + kChunk < H.dp && ldg(H.P + c0 + kChunk - 1) < umin) c0 += kChunk;
-        H.c0 = c0;
-        hash_build(H, lane);
+        const uint32_t dp = fw_smem[woff + kCtlWord + 2];
+        uint32_t c0 = fw_smem[woff + kCtlWord + 0] + fw_smem[woff + kCtlWord + 1];
+        while (c0 + kChunk < dp && ldg(P + c0 + kChunk - 1) < umin) c0 += kChunk;
+        const HashState hs = hash_build(P, c0, dp, woff, lane);
+        hshift = hs.hshift;
+        lim = hs.lim;
+        full = 0;
+        uint32_t here = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            if (((need >> e) & 1) && u[e] <= lim) {
+                here |= 1u << e;
+                const uint4 q = bucket_at(woff, hbucket(u[e], hshift));
+                if (bucket_has(q, u[e])) mem |= 1u << e;
+                else if (q.w != kEmpty) full |= 1u << e;
+            }
+        }
+        need &= ~here;
     }
 }
 
 // 4 independent branchless binary searches over P[0, dp) (global memory).
-__device__ __forceinline__ uint32_t member4_bsearch(const uint32_t *__restrict__ P, uint32_t dp,
-                                                   const uint32_t u[4], uint32_t need) {
+__device__ FW_COLD uint32_t member4_bsearch(const uint32_t *__restrict__ P, uint32_t dp,
+                                                uint32_t u0, uint32_t u1, uint32_t u2,
+                                                uint32_t u3, uint32_t need) {
+    const uint32_t u[4] = {u0, u1, u2, u3};
     uint32_t b[4] = {0, 0, 0, 0};
     uint32_t n = dp;
     while (n > 1) {
@@ -443,11 +462,9 @@ __device__ __forceinline__ uint32_t member4_bsearch(const uint32_t *__restrict__
     return mem;
 }
 
-// KMODE 1: k == 32 (lane bases of this lane's 4 slots live in registers:
-//          slot e always maps to logical lane (4p+e-off) mod 32, its counter
-//          advances by 4 per 128-element tile);
-// KMODE 2: power-of-two 4 <= k <= 256, bases staged in shared memory with a
-//          bank-conflict-free layout (j & 3) * k/4 + j/4;
+// KMODE 2: power-of-two 4 <= k <= 256: lane bases staged in shared memory,
+//          bank-conflict-free layout (j & 3) * k/4 + j/4 (slot e of lane p
+//          reads row (e-off)&3, column (32t+p+..) & (k/4-1));
 // KMODE 0: any other k (bases recomputed per element).
 template <int KMODE>
 __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
@@ -455,58 +472,40 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
     const uint32_t off = (uint32_t)(s.elo & 3);
-    const uint32_t kq = k >> 2;            // KMODE 2: bases per row
-    const uint32_t kshift = 31 - __clz(k);  // log2 k for powers of two
-    const uint32_t sbw = woff + kHashSlots;  // word offset of the staged bases
-    uint64_t word[4];
-    if constexpr (KMODE == 1) {
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const int32_t i = lane * 4 + e - (int32_t)off;
-            word[e] = lane_base(a, s, (uint32_t)i & 31u) + (uint64_t)(int64_t)(i >> 5) * GOLDEN;
-        }
-    }
     if constexpr (KMODE == 2) {
-        const uint32_t nl = min(k, deg);
-        uint64_t *sb = reinterpret_cast<uint64_t *>(fw_smem + sbw);
+        const uint32_t nl = min(k, deg), kq = k >> 2;
+        uint64_t *sb = reinterpret_cast<uint64_t *>(fw_smem + woff + kHashSlots);
         for (uint32_t j = lane; j < nl; j += 32) sb[(j & 3) * kq + (j >> 2)] = lane_base(a, s, j);
     }
-    HashWin H;
-    H.P = a.tgt + s.plo;
-    H.tab = woff;
-    H.dp = (uint32_t)(s.phi - s.plo);
-    const bool use_hash = H.dp <= a.merge_ratio * deg + 2 * kChunk;
+    const uint32_t *P = a.tgt + s.plo;
+    const uint32_t dp = (uint32_t)(s.phi - s.plo);
+    const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
+    uint32_t lim = 0, hshift = 0;
     if (use_hash) {
-        H.c0 = 0;
-        hash_build(H, lane);  // (ends with __syncwarp: staged bases visible too)
+        const HashState hs = hash_build(P, 0, dp, woff, lane);
+        hshift = hs.hshift;
+        lim = hs.lim;
     } else {
         __syncwarp();
     }
     const uint32_t span = deg + off;
     const uint32_t ntiles = (span + 127) >> 7;
-    const uint4 *T4 = reinterpret_cast<const uint4 *>(a.tgt + (s.elo - off));
-    const float4 *W4 = reinterpret_cast<const float4 *>(a.w + (s.elo - off));
-    const bool weighted = a.weighted != 0;
-    const double inv_a = a.inv_a, inv_b = a.inv_b;
+    const int64_t ebase = s.elo - off;
     uint4 nu = make_uint4(0, 0, 0, 0);
-    float4 nw = make_float4(1.f, 1.f, 1.f, 1.f);
-    if ((uint32_t)lane * 4 < span) {
-        nu = ldg(T4 + lane);
-        if (weighted) nw = ldg(W4 + lane);
-    }
+    if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + lane);
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
     for (uint32_t t = 0; t < ntiles; t++) {
+        const uint32_t x = t * 128 + lane * 4;  // slot of element 0 of this lane
         const uint4 u4 = nu;
-        const float4 w4 = nw;
-        const uint32_t nx = (t + 1) * 128 + lane * 4;
-        if (nx < span) {  // prefetch the next tile
-            nu = ldg(T4 + (nx >> 2));
-            if (weighted) nw = ldg(W4 + (nx >> 2));
+        float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
+        if (x < span) {
+            if (a.weighted) w4 = ldg(reinterpret_cast<const float4 *>(a.w + ebase) + (x >> 2));
+            if (x + 128 < span)  // prefetch the next tile's targets
+                nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + ((x + 128) >> 2));
         }
-        const int32_t i0 = (int32_t)(t * 128 + lane * 4) - (int32_t)off;
+        const int32_t i0 = (int32_t)x - (int32_t)off;
         const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
-        const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
         uint32_t vmask = 0xFu;
         if (i0 < 0) vmask &= 0xFu << (-i0);
         const int32_t rem = (int32_t)deg - i0;
@@ -514,46 +513,64 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         uint32_t pmask = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) pmask |= (u[e] == prev ? 1u : 0u) << e;
+        uint32_t mem = 0;
         const uint32_t need = vmask & ~pmask;
-        const uint32_t mem = use_hash ? member4_hash(H, u, need, lane)
-                                      : member4_bsearch(H.P, H.dp, u, need);
+        if (use_hash) {
+            uint32_t here = 0, full = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                if (((need >> e) & 1) && u[e] <= lim) {
+                    here |= 1u << e;
+                    const uint4 q = bucket_at(woff, hbucket(u[e], hshift));
+                    if (bucket_has(q, u[e])) mem |= 1u << e;
+                    else if (q.w != kEmpty) full |= 1u << e;
+                }
+            }
+            const uint32_t pend = need & ~here;
+            if (__any_sync(FULL, full | pend)) {
+                const SlowRet sr = member4_slow(P, woff, u[0], u[1], u[2], u[3], full, pend,
+                                                hshift, lim, lane);
+                mem |= sr.mem;
+                hshift = sr.hshift;
+                lim = sr.lim;
+            }
+        } else {
+            mem = member4_bsearch(P, dp, u[0], u[1], u[2], u[3], need);
+        }
+        const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
         double wv[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            const double bse = ((pmask >> e) & 1) ? inv_a : (((mem >> e) & 1) ? 1.0 : inv_b);
-            const double x = weighted ? __dmul_rn(bse, (double)wf[e]) : bse;
-            wv[e] = ((vmask >> e) & 1) ? x : 0.0;
+            const double bse = ((pmask >> e) & 1) ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
+            const double xw = a.weighted ? __dmul_rn(bse, (double)wf[e]) : bse;
+            wv[e] = ((vmask >> e) & 1) ? xw : 0.0;
         }
         const double p1 = __dadd_rn(wv[0], wv[1]);
         const double p2 = __dadd_rn(p1, wv[2]);
         const double p3 = __dadd_rn(p2, wv[3]);
         const double incl = warp_incl_scan_d(p3, lane);
-        const double excl = __dadd_rn(incl, -p3);  // exact (EXACT mode)
-        const double base = __dadd_rn(carry, excl);
+        const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
+        carry = __dadd_rn(carry, shfl_d(incl, 31));
         const double pre[4] = {wv[0], p1, p2, p3};
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const uint32_t i = (uint32_t)(i0 + e);
             uint64_t wd;
-            if constexpr (KMODE == 1) {
-                wd = word[e];
-                word[e] += 4 * GOLDEN;
-            } else if constexpr (KMODE == 2) {
-                const uint32_t j = i & (k - 1);
-                const uint64_t b = reinterpret_cast<const uint64_t *>(fw_smem + sbw)
-                    [((uint32_t)(e - (int)off) & 3u) * kq + (j >> 2)];
-                wd = b + (uint64_t)(i >> kshift) * GOLDEN;
+            if constexpr (KMODE == 2) {
+                const uint32_t kq = k >> 2;
+                const uint64_t *sb = reinterpret_cast<const uint64_t *>(fw_smem + woff + kHashSlots);
+                wd = sb[((uint32_t)(e - (int)off) & 3u) * kq + ((i >> 2) & (kq - 1))] +
+                     (uint64_t)(i >> (31 - __clz(k))) * GOLDEN;
             } else {
                 wd = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
             }
             const double r = u01_word(wd);
-            const double P = __dadd_rn(base, pre[e]);
-            if (wv[e] > 0.0 && __dmul_rn(r, P) < wv[e]) {
+            const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
+            if (wv[e] > 0.0 && Pr < wv[e]) {
                 cand = i + 1;
                 cand_u = u[e];
             }
         }
-        carry = __dadd_rn(carry, shfl_d(incl, 31));
     }
     const uint32_t sel = __reduce_max_sync(FULL, cand);
     const unsigned who = __ballot_sync(FULL, cand == sel);
@@ -602,7 +619,6 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks)
 walk_kernel(const WalkArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t woff = (threadIdx.x >> 5) * kWarpSmemWords;
-    uint32_t *wsm = fw_smem + woff;
     // per-warp RunStats counters live in shared memory (registers are the
     // scarce resource in the sampler loops); every lane keeps the same value
     // in flight, lane 0 owns the slot.
@@ -674,7 +690,7 @@ walk_kernel(const WalkArgs a) {
                 stat_add(st, ST_COLLECTIVES, 2 * chunks, lane);
                 stat_add(st, ST_EDGES, s.deg, lane);
             } else {
-                sel = zprs_warp<APP, EXACT>(a, s, k, lane, wsm);
+                sel = zprs_warp<APP, EXACT>(a, s, k, lane, woff);
                 stat_add(st, ST_COLLECTIVES, 2, lane);
                 stat_add(st, ST_EDGES, 2 * s.deg, lane);
             }

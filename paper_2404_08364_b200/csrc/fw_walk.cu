@@ -369,8 +369,19 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t
     }
     __syncwarp();
     const uint32_t *src = P + c0;
-    for (uint32_t x = lane; x < cn; x += 32) {
-        const uint32_t key = ldg(src + x);
+    // all of this lane's keys are requested before the first insert (the
+    // loads are independent; inserting as they arrive serialised them)
+    constexpr int kKeys = kChunk / 32;
+    uint32_t keys[kKeys];
+#pragma unroll
+    for (int r = 0; r < kKeys; r++) {
+        const uint32_t x = r * 32 + lane;
+        keys[r] = x < cn ? ldg(src + x) : kEmpty;
+    }
+#pragma unroll
+    for (int r = 0; r < kKeys; r++) {
+        const uint32_t key = keys[r];
+        if (key == kEmpty) continue;
         uint32_t b = hbucket(key, shift);
         for (;;) {
             uint32_t old = kEmpty;

@@ -30,7 +30,9 @@ def replicate_csr(arrays, shapes_dtypes, src=0, device=None):
     freshly allocated tensors of `shapes_dtypes` [(numel, dtype), ...]."""
     rank = dist.get_rank()
     if rank != src:
-        arrays = [None if sd is None else torch.empty(sd[0], dtype=sd[1], device=device)
+        # 4 spare elements: the walk kernel reads 16-byte tiles of targets/weights
+        arrays = [None if sd is None else
+                  torch.empty(sd[0] + 4, dtype=sd[1], device=device)[:sd[0]]
                   for sd in shapes_dtypes]
     for t in arrays:
         if t is not None:

@@ -219,7 +219,9 @@ def _upload(g, device):
 class DeviceGraph:
     """A CSR resident in HBM (torch tensors as the allocator), reusable
     across calls.  Arrays: offsets int64, targets int32 (bit-cast uint32),
-    weights float32, labels uint8 or None."""
+    weights float32, labels uint8 or None.  targets/weights must stay
+    readable 16 bytes past their end (the walk kernel loads 16-byte tiles);
+    to_device() and rmat_graph_device() allocate that padding."""
 
     def __init__(self, vertex_count, edge_count, offsets, targets, weights, labels=None,
                  device=0):
@@ -274,8 +276,14 @@ def _replicate(dg, device):
     devices are peers) and a handle on the new device."""
     import torch
     dev = torch.device("cuda", device)
-    arrs = [None if t is None else t.to(dev, non_blocking=True)
-            for t in (dg.offsets, dg.targets, dg.weights, dg.labels)]
+    arrs = []
+    for t, pad in ((dg.offsets, 0), (dg.targets, 4), (dg.weights, 4), (dg.labels, 0)):
+        if t is None:
+            arrs.append(None)
+            continue
+        c = torch.empty(t.numel() + pad, dtype=t.dtype, device=dev)[:t.numel()]
+        c.copy_(t, non_blocking=True)
+        arrs.append(c)
     torch.cuda.synchronize(dev)
     rep = DeviceGraph(dg.vertex_count, dg.edge_count, *arrs, device=device)
     return rep._handle
@@ -285,11 +293,16 @@ def to_device(g, device=0):
     """Upload a host Graph once and keep it resident (DeviceGraph)."""
     import torch
     dev = torch.device("cuda", device)
-    tg = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).to(dev)  # noqa: E731
+    def tg(a, dt, pad=0):
+        host = torch.from_numpy(np.ascontiguousarray(a).view(dt))
+        out = torch.empty(host.numel() + pad, dtype=host.dtype, device=dev)[:host.numel()]
+        out.copy_(host)
+        return out
+
     lab = None if g.labels is None else tg(np.asarray(g.labels, np.uint8), np.uint8)
     return DeviceGraph(g.vertex_count, g.edge_count, tg(np.asarray(g.offsets, np.int64), np.int64),
-                       tg(np.asarray(g.targets, np.uint32), np.int32),
-                       tg(np.asarray(g.weights, np.float32), np.float32), lab, device=device)
+                       tg(np.asarray(g.targets, np.uint32), np.int32, 4),
+                       tg(np.asarray(g.weights, np.float32), np.float32, 4), lab, device=device)
 
 
 class _Session:

@@ -101,9 +101,31 @@ def rmat_graph(scale, edge_factor=16, seed=GRAPH_SEED, labels=True,
     return Graph(V, E, offsets, targets, w, lab)
 
 
+def _sort_keys(key, V, max_sort):
+    """Sort int64 (src << 32 | dst) keys; above `max_sort` elements the sort
+    is split into src-range buckets (each sorted separately, concatenated),
+    keeping every torch.sort call well inside 32-bit index limits."""
+    import torch
+    E = key.numel()
+    nb = max(1, -(-E // max_sort))
+    if nb == 1:
+        return torch.sort(key)[0]
+    out = torch.empty_like(key)
+    pos = 0
+    for b in range(nb):
+        lo, hi = (V * b // nb) << 32, (V * (b + 1) // nb) << 32
+        sel = key[(key >= lo) & (key < hi)]
+        sel = torch.sort(sel)[0]
+        out[pos:pos + sel.numel()] = sel
+        pos += sel.numel()
+        del sel
+    assert pos == E
+    return out
+
+
 def rmat_graph_device(scale, edge_factor=16, seed=GRAPH_SEED, labels=True,
                       weight_seed=WEIGHT_SEED, label_seed=LABEL_SEED, label_count=5,
-                      device=0):
+                      device=0, max_sort=1 << 28):
     """Device build: hash-generated edges (sm_100a kernels in libflowwalk.so),
     torch.sort as plumbing for the (src, dst) order, weights/labels by CSR
     position.  Returns a DeviceGraph whose arrays equal rmat_graph(...)'s."""
@@ -127,16 +149,18 @@ def rmat_graph_device(scale, edge_factor=16, seed=GRAPH_SEED, labels=True,
         del uv
         key = torch.cat([(u << 32) | v, (v << 32) | u])
         del u, v
-        key, _ = torch.sort(key)
+        key = _sort_keys(key, V, max_sort)
         src = key >> 32
         counts = torch.bincount(src, minlength=V)
         del src
         offsets = torch.zeros(V + 1, dtype=torch.int64, device=dev)
         torch.cumsum(counts, 0, out=offsets[1:])
         del counts
-        targets = (key & 0xFFFFFFFF).to(torch.int32)
+        # +4 elements: the walk kernel reads 16-byte tiles (DeviceGraph contract)
+        targets = torch.empty(E + 4, dtype=torch.int32, device=dev)[:E]
+        targets.copy_(key & 0xFFFFFFFF)
         del key
-        weights = torch.empty(E, dtype=torch.float32, device=dev)
+        weights = torch.empty(E + 4, dtype=torch.float32, device=dev)[:E]
         _lib.check(lib.fw_synth_weights_device(weight_seed, 0, E, weights.data_ptr(), stream))
         lab = None
         if labels:

@@ -144,14 +144,22 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def profiled_traffic(workload):
-    """dram bytes per launch of the walk kernel from the committed ncu capture."""
+def profiled_traffic(workload, alg_bytes):
+    """DRAM bytes per launch of the walk kernel, from the committed ncu
+    --set full capture of this workload (profiles/walk_traffic.json).  The
+    capture runs a smaller launch (fewer queries) to keep ncu's replays
+    short, so it is scaled by the ratio of algorithmic bytes."""
     try:
         with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as fh:
-            d = json.load(fh)
-        return d.get(workload)
+            d = json.load(fh).get(workload)
     except (OSError, ValueError):
-        return None
+        return None, None
+    if not d or not d.get("alg_bytes"):
+        return None, None
+    return (d["dram_bytes"] * alg_bytes / d["alg_bytes"],
+            f"ncu --set full of a {d['queries']}-query launch ({d['report']}): "
+            f"{d['dram_bytes'] / d['alg_bytes']:.3f} DRAM bytes per algorithmic byte, "
+            f"scaled to this launch")
 
 
 # ---------------------------------------------------------------------------
@@ -399,9 +407,10 @@ def bench_ours(args):
     mean_launch_s = (my_ms / args.steps) / 1000.0
     achieved = (alg_bytes / args.steps) / mean_launch_s / 1e9
     workload = workload_name(args, app)
+    traffic, traffic_basis = profiled_traffic(workload, alg_bytes / args.steps)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_kind": peak_kind,
-                "traffic": profiled_traffic(workload),
+                "traffic": traffic, "traffic_basis": traffic_basis,
                 "alg_bytes_per_launch": alg_bytes // args.steps,
                 "kernel": "fw::walk_kernel (persistent, 1 launch per step)"}
 

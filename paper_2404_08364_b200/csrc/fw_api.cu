@@ -372,6 +372,10 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     a.stop_prob = app->stop_prob;
     a.inv_a = app->inv_a;
     a.inv_b = app->inv_b;
+    a.fac[0] = app->inv_b;
+    a.fac[1] = 1.0;
+    a.fac[2] = app->inv_a;
+    a.fac[3] = app->inv_a;
     a.k_small = eng->k_small;
     a.k_big = eng->k_big;
     a.d_t = eng->d_t;

@@ -319,13 +319,21 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
     const int hi = __shfl_sync(FULL, __double2hiint(x), src);
     return __hiloint2double(hi, lo);
 }
-__device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double o = shfl_up_d(v, d);
-        if (lane >= d) v = __dadd_rn(v, o);
-    }
+// Predicated DADD (no FSEL pair on the ALU pipe, which is the binding pipe
+// of the sampler loops).
+template <int D>
+__device__ __forceinline__ double scan_round(double v, int lane) {
+    const double o = shfl_up_d(v, D);
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %1, %2;\n\t@p add.rn.f64 %0, %0, %3;\n\t}"
+        : "+d"(v) : "r"(lane), "n"(D), "d"(o));
     return v;
+}
+__device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
+    v = scan_round<1>(v, lane);
+    v = scan_round<2>(v, lane);
+    v = scan_round<4>(v, lane);
+    v = scan_round<8>(v, lane);
+    return scan_round<16>(v, lane);
 }
 
 // Bucketed open addressing in the warp's shared-memory slice: 4 slots (16
@@ -549,13 +557,16 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         } else {
             mem = member4_bsearch(P, dp, u[0], u[1], u[2], u[3], need);
         }
+        // invalid slots get weight 0 before the conversion (one float select
+        // instead of a double select); the factor comes from the launch's
+        // constant table fac[2*is_prev + is_member] = {1/b, 1, 1/a, 1/a}
         const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
         double wv[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            const double bse = ((pmask >> e) & 1) ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
-            const double xw = a.weighted ? __dmul_rn(bse, (double)wf[e]) : bse;
-            wv[e] = ((vmask >> e) & 1) ? xw : 0.0;
+            const float w0 = ((vmask >> e) & 1) ? (a.weighted ? wf[e] : 1.0f) : 0.0f;
+            const uint32_t fi = (((pmask >> e) & 1) << 1) | ((mem >> e) & 1);
+            wv[e] = __dmul_rn(a.fac[fi], (double)w0);
         }
         const double p1 = __dadd_rn(wv[0], wv[1]);
         const double p2 = __dadd_rn(p1, wv[2]);

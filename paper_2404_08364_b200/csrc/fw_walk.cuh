@@ -33,6 +33,7 @@ struct WalkArgs {
     const int64_t *schema;  // device copy
     int32_t weighted;
     double stop_prob, inv_a, inv_b;
+    double fac[4];  // node2vec factor by 2*is_prev + is_member: {1/b, 1, 1/a, 1/a}
     int64_t k_small, k_big, d_t;
     uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
     uint32_t merge_ratio;  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch

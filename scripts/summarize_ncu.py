@@ -66,7 +66,7 @@ METRICS = [
 ]
 
 
-def full(rep, out, traffic_key=None):
+def full(rep, out, traffic_key=None, alg_bytes=None, queries=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
@@ -93,10 +93,14 @@ def full(rep, out, traffic_key=None):
             tb = rd * scale.get(u.get("dram__bytes_read.sum"), 1) + \
                 wr * scale.get(u.get("dram__bytes_write.sum"), 1)
             fh.write(f"\nDRAM traffic per launch: {tb:.4g} bytes\n\n")
+            if alg_bytes:
+                fh.write(f"Algorithmic bytes of this launch: {alg_bytes:.4g} "
+                         f"(DRAM traffic / algorithmic = {tb / alg_bytes:.3f})\n\n")
             if traffic_key:
                 p = os.path.join(ROOT, "profiles", "walk_traffic.json")
                 cur = json.load(open(p)) if os.path.exists(p) else {}
-                cur[traffic_key] = tb
+                cur[traffic_key] = {"dram_bytes": tb, "alg_bytes": alg_bytes, "queries": queries,
+                                    "report": os.path.basename(rep)}
                 json.dump(cur, open(p, "w"), indent=1)
     print(open(out).read())
 
@@ -106,5 +110,6 @@ if __name__ == "__main__":
     if mode == "launches":
         launches(src, dst)
     else:
-        key = sys.argv[sys.argv.index("--traffic-key") + 1] if "--traffic-key" in sys.argv else None
-        full(src, dst, key)
+        def opt(name, conv=str):
+            return conv(sys.argv[sys.argv.index(name) + 1]) if name in sys.argv else None
+        full(src, dst, opt("--traffic-key"), opt("--alg-bytes", float), opt("--queries", int))

@@ -14,7 +14,9 @@ constexpr uint32_t kHashSlots = 1024;
 constexpr uint32_t kChunk = 256;  // N(prev) entries hashed at a time (load <= 1/4)
 constexpr uint32_t kStatsWord = kHashSlots + 2 * 256;    // 8 x u64 RunStats counters
 constexpr uint32_t kCtlWord = kStatsWord + 2 * 8;       // hash window control words
-constexpr uint32_t kWarpSmemWords = kCtlWord + 4;
+constexpr uint32_t kMemTiles = 32;                      // node2vec membership-bit ring (tiles)
+constexpr uint32_t kMemRingWord = kCtlWord + 4;
+constexpr uint32_t kWarpSmemWords = kMemRingWord + kMemTiles * 4;
 constexpr int kWalkSmemBytes = (kWalkThreads / 32) * kWarpSmemWords * 4;
 
 // Kernel arguments (passed by value through the constant bank).
@@ -36,7 +38,8 @@ struct WalkArgs {
     double fac[4];  // node2vec factor by 2*is_prev + is_member: {1/b, 1, 1/a, 1/a}
     int64_t k_small, k_big, d_t;
     uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
-    uint32_t merge_ratio;  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
+    uint32_t merge_ratio;
+    uint32_t n2v_mode;  // 0: two-pass early-exit DPRS (default), 1: single forward pass  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };

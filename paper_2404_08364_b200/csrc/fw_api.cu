@@ -383,8 +383,6 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     {
         const char *mr = getenv("FW_MERGE_RATIO");
         a.merge_ratio = mr ? (uint32_t)atoi(mr) : 32u;
-        const char *nm = getenv("FW_N2V_MODE");
-        a.n2v_mode = nm ? (uint32_t)atoi(nm) : 0u;
     }
     a.stats = (long long *)d_stats;
     unsigned slot;

@@ -602,187 +602,6 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
     return sel;
 }
 
-// ---------------------------------------------------------------------------
-// Node2Vec DPRS, exact order, two passes with early exit (default).
-//
-// The DPRS result is the LAST accepted element in natural order.  When all
-// partial sums are exact (EXACT), P_i = W - (weight after i) for the total
-// W, so the elements can be tested from the end backwards and the first
-// acceptance found is the answer: on average only about half of the
-// elements ever need a random draw (the reference's counter hash is the
-// dominant per-element cost).
-//   pass A (forward): membership + weights, no RNG; total W; membership
-//           bits of the last kMemTiles tiles are kept in shared memory;
-//   pass B (backward): weights again (membership from the ring, or a
-//           binary search in N(prev) beyond it), exact prefixes from the
-//           running suffix, draws, stop at the first tile with an accept.
-// Every P_i is the same exact value the reference's forward sum produces,
-// so the selection is bit-identical.
-// ---------------------------------------------------------------------------
-template <int KMODE>
-__device__ uint32_t dprs_n2v_exact2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
-                                    uint32_t woff, uint32_t &sel_u) {
-    const uint32_t deg = s.deg;
-    const uint32_t prev = (uint32_t)s.prev;
-    const uint32_t off = (uint32_t)(s.elo & 3);
-    if constexpr (KMODE == 2) {
-        const uint32_t nl = min(k, deg), kq = k >> 2;
-        uint64_t *sb = reinterpret_cast<uint64_t *>(fw_smem + woff + kHashSlots);
-        for (uint32_t j = lane; j < nl; j += 32) sb[(j & 3) * kq + (j >> 2)] = lane_base(a, s, j);
-    }
-    const uint32_t *P = a.tgt + s.plo;
-    const uint32_t dp = (uint32_t)(s.phi - s.plo);
-    const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
-    uint32_t lim = 0, hshift = 0;
-    if (use_hash) {
-        const HashState hs = hash_build(P, 0, dp, woff, lane);
-        hshift = hs.hshift;
-        lim = hs.lim;
-    } else {
-        __syncwarp();
-    }
-    const uint32_t span = deg + off;
-    const uint32_t ntiles = (span + 127) >> 7;
-    const int64_t ebase = s.elo - off;
-    const uint4 *T4 = reinterpret_cast<const uint4 *>(a.tgt + ebase);
-    const float4 *W4 = reinterpret_cast<const float4 *>(a.w + ebase);
-    uint32_t *ring = fw_smem + woff + kMemRingWord;
-    // ---- pass A ----------------------------------------------------------
-    double lane_w = 0.0;
-    uint4 nu = make_uint4(0, 0, 0, 0);
-    if ((uint32_t)lane * 4 < span) nu = ldg(T4 + lane);
-    for (uint32_t t = 0; t < ntiles; t++) {
-        const uint32_t x = t * 128 + lane * 4;
-        const uint4 u4 = nu;
-        float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (x < span) {
-            if (a.weighted) w4 = ldg(W4 + (x >> 2));
-            if (x + 128 < span) nu = ldg(T4 + ((x + 128) >> 2));
-        }
-        const int32_t i0 = (int32_t)x - (int32_t)off;
-        const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
-        uint32_t vmask = 0xFu;
-        if (i0 < 0) vmask &= 0xFu << (-i0);
-        const int32_t rem = (int32_t)deg - i0;
-        if (rem < 4) vmask &= rem <= 0 ? 0u : (1u << rem) - 1;
-        uint32_t pmask = 0;
-#pragma unroll
-        for (int e = 0; e < 4; e++) pmask |= (u[e] == prev ? 1u : 0u) << e;
-        uint32_t mem = 0;
-        const uint32_t need = vmask & ~pmask;
-        if (use_hash) {
-            uint32_t here = 0, full = 0;
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                if (((need >> e) & 1) && u[e] <= lim) {
-                    here |= 1u << e;
-                    const uint4 q = bucket_at(woff, hbucket(u[e], hshift));
-                    if (bucket_has(q, u[e])) mem |= 1u << e;
-                    else if (q.w != kEmpty) full |= 1u << e;
-                }
-            }
-            const uint32_t pend = need & ~here;
-            if (__any_sync(FULL, full | pend)) {
-                const SlowRet sr = member4_slow(P, woff, u[0], u[1], u[2], u[3], full, pend,
-                                                hshift, lim, lane);
-                mem |= sr.mem;
-                hshift = sr.hshift;
-                lim = sr.lim;
-            }
-        } else {
-            mem = member4_bsearch(P, dp, u[0], u[1], u[2], u[3], need);
-        }
-        const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const float w0 = ((vmask >> e) & 1) ? (a.weighted ? wf[e] : 1.0f) : 0.0f;
-            const uint32_t fi = (((pmask >> e) & 1) << 1) | ((mem >> e) & 1);
-            lane_w = __dadd_rn(lane_w, __dmul_rn(a.fac[fi], (double)w0));
-            const unsigned b = __ballot_sync(FULL, (mem >> e) & 1);
-            if (lane == e) ring[(t & (kMemTiles - 1)) * 4 + e] = b;
-        }
-    }
-    const double W = warp_sum(lane_w);  // exact
-    __syncwarp();
-    // ---- pass B ----------------------------------------------------------
-    double S = 0.0;  // weight of the tiles after the current one
-    uint32_t sel = 0, selu = 0;
-    const uint32_t ring_lo = ntiles > kMemTiles ? ntiles - kMemTiles : 0;
-    for (int32_t t = (int32_t)ntiles - 1; t >= 0; t--) {
-        const uint32_t x = (uint32_t)t * 128 + lane * 4;
-        uint4 u4 = make_uint4(0, 0, 0, 0);
-        float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (x < span) {
-            u4 = ldg(T4 + (x >> 2));
-            if (a.weighted) w4 = ldg(W4 + (x >> 2));
-        }
-        const int32_t i0 = (int32_t)x - (int32_t)off;
-        const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
-        uint32_t vmask = 0xFu;
-        if (i0 < 0) vmask &= 0xFu << (-i0);
-        const int32_t rem = (int32_t)deg - i0;
-        if (rem < 4) vmask &= rem <= 0 ? 0u : (1u << rem) - 1;
-        uint32_t pmask = 0;
-#pragma unroll
-        for (int e = 0; e < 4; e++) pmask |= (u[e] == prev ? 1u : 0u) << e;
-        uint32_t mem = 0;
-        if ((uint32_t)t >= ring_lo) {
-#pragma unroll
-            for (int e = 0; e < 4; e++)
-                mem |= ((ring[((uint32_t)t & (kMemTiles - 1)) * 4 + e] >> lane) & 1u) << e;
-        } else {
-            mem = member4_bsearch(P, dp, u[0], u[1], u[2], u[3], vmask & ~pmask);
-        }
-        const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
-        double wv[4];
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const float w0 = ((vmask >> e) & 1) ? (a.weighted ? wf[e] : 1.0f) : 0.0f;
-            const uint32_t fi = (((pmask >> e) & 1) << 1) | ((mem >> e) & 1);
-            wv[e] = __dmul_rn(a.fac[fi], (double)w0);
-        }
-        const double a3 = wv[3];                  // weight after element 2 (in lane)
-        const double a2 = __dadd_rn(wv[2], a3);   // after element 1
-        const double a1 = __dadd_rn(wv[1], a2);   // after element 0
-        const double lt = __dadd_rn(wv[0], a1);   // lane total
-        const double incl = warp_incl_scan_d(lt, lane);
-        const double tile = shfl_d(incl, 31);
-        // prefix through element 3 of this lane = W - S - (lanes after this one)
-        const double p3 = __dadd_rn(__dadd_rn(W, -S), -__dadd_rn(tile, -incl));
-        const double pre[4] = {__dadd_rn(p3, -a1), __dadd_rn(p3, -a2), __dadd_rn(p3, -a3), p3};
-        uint32_t cand = 0, cu = 0;
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const uint32_t i = (uint32_t)(i0 + e);
-            uint64_t wd;
-            if constexpr (KMODE == 2) {
-                const uint32_t kq = k >> 2;
-                const uint64_t *sb = reinterpret_cast<const uint64_t *>(fw_smem + woff + kHashSlots);
-                wd = sb[((uint32_t)(e - (int)off) & 3u) * kq + ((i >> 2) & (kq - 1))] +
-                     (uint64_t)(i >> (31 - __clz(k))) * GOLDEN;
-            } else {
-                wd = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
-            }
-            const double r = u01_word(wd);
-            if (wv[e] > 0.0 && __dmul_rn(r, pre[e]) < wv[e]) {
-                cand = i + 1;
-                cu = u[e];
-            }
-        }
-        const uint32_t best = __reduce_max_sync(FULL, cand);
-        if (best) {
-            sel = best;
-            const unsigned who = __ballot_sync(FULL, cand == best);
-            selu = __shfl_sync(FULL, cu, __ffs(who) - 1);
-            break;
-        }
-        S = __dadd_rn(S, tile);
-    }
-    sel_u = selu;
-    __syncwarp();  // table and ring are rewritten by the next step
-    return sel;
-}
-
 template <int APP>
 __device__ uint32_t dprs_warp_ordered(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane) {
     const uint32_t deg = s.deg;
@@ -878,14 +697,10 @@ walk_kernel(const WalkArgs a) {
             if constexpr (SAMPLER == SAMPLER_DPRS) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
-                        const bool kp = k >= 4 && k <= 256 && (k & (k - 1)) == 0;
-                        if (a.n2v_mode == 0) {
-                            sel = kp ? dprs_n2v_exact2<2>(a, s, k, lane, woff, sel_u)
-                                     : dprs_n2v_exact2<0>(a, s, k, lane, woff, sel_u);
-                        } else {
-                            sel = kp ? dprs_n2v_exact<2>(a, s, k, lane, woff, sel_u)
-                                     : dprs_n2v_exact<0>(a, s, k, lane, woff, sel_u);
-                        }
+                        if (k >= 4 && k <= 256 && (k & (k - 1)) == 0)
+                            sel = dprs_n2v_exact<2>(a, s, k, lane, woff, sel_u);
+                        else
+                            sel = dprs_n2v_exact<0>(a, s, k, lane, woff, sel_u);
                         have_u = true;
                     } else {
                         sel = dprs_warp_exact<APP>(a, s, k, lane);

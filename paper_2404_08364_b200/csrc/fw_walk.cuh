@@ -14,9 +14,7 @@ constexpr uint32_t kHashSlots = 1024;
 constexpr uint32_t kChunk = 256;  // N(prev) entries hashed at a time (load <= 1/4)
 constexpr uint32_t kStatsWord = kHashSlots + 2 * 256;    // 8 x u64 RunStats counters
 constexpr uint32_t kCtlWord = kStatsWord + 2 * 8;       // hash window control words
-constexpr uint32_t kMemTiles = 32;                      // node2vec membership-bit ring (tiles)
-constexpr uint32_t kMemRingWord = kCtlWord + 4;
-constexpr uint32_t kWarpSmemWords = kMemRingWord + kMemTiles * 4;
+constexpr uint32_t kWarpSmemWords = kCtlWord + 4;
 constexpr int kWalkSmemBytes = (kWalkThreads / 32) * kWarpSmemWords * 4;
 
 // Kernel arguments (passed by value through the constant bank).

@@ -60,6 +60,8 @@ def parse_args():
                         "strong: one query set partitioned over the GPUs")
     p.add_argument("--gather", action="store_true",
                    help="after timing, gather path segments to rank 0 (timed separately)")
+    p.add_argument("--dump-gather", default=None,
+                   help="with --gather: rank 0 saves the gathered paths (.npz) for tests")
     return p.parse_args()
 
 
@@ -285,10 +287,19 @@ def bench_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    # one GPU per rank over NCCL; with fewer GPUs than ranks (functional
+    # testing on a 1-GPU box) the ranks share devices and talk over gloo
+    backend = "nccl" if ndev >= world else "gloo"
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # collective tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     lib = _lib.load()
     app = app_config(args)
     labels = args.app == "metapath"
@@ -305,7 +316,17 @@ def bench_ours(args):
             ([(E_, torch.uint8)] if labels else [])
         torch.cuda.synchronize()
         t_rep = time.perf_counter()
-        arrs = fwd.replicate_csr(arrs if rank == 0 else None, sd, src=0, device=dev)
+        if backend == "nccl":
+            arrs = fwd.replicate_csr(arrs if rank == 0 else None, sd, src=0, device=dev)
+        else:
+            host = fwd.replicate_csr([t.cpu() for t in arrs] if rank == 0 else None, sd, src=0,
+                                     device=cdev)
+            if rank != 0:
+                arrs = []
+                for t, pad in zip(host, (0, 4, 4, 0)):
+                    d = torch.empty(t.numel() + pad, dtype=t.dtype, device=dev)[:t.numel()]
+                    d.copy_(t)
+                    arrs.append(d)
         torch.cuda.synchronize()
         t_rep = time.perf_counter() - t_rep
         if rank != 0:
@@ -358,15 +379,14 @@ def bench_ours(args):
     if world > 1 and args.gather and args.scaling == "strong":
         torch.cuda.synchronize()
         t_g = time.perf_counter()
-        fwd.gather_paths(seq, lens, n_total, L, dst=0)
+        gathered = fwd.gather_paths(seq.to(cdev), lens.to(cdev), n_total, L, dst=0)
         torch.cuda.synchronize()
         gather_ms = 1000 * (time.perf_counter() - t_g)
-    my_ms = sum(launch_ms)
-    st = stats.cpu().numpy()
-    sampled = int(st[6])
-    alg_bytes = int(st[7])
-    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-    tot = torch.tensor([sampled], dtype=torch.int64, device=dev)
+        if args.dump_gather and rank == 0:  # consumed by tests/test_gpu_parity.py
+            np.savez(args.dump_gather, seq=gathered[0].cpu().numpy().view(np.uint32),
+                     lens=gathered[1].cpu().numpy().view(np.uint32))
+    t = torch.tensor([my_ms], dtype=torch.float64, device=cdev)
+    tot = torch.tensor([sampled], dtype=torch.int64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
@@ -393,8 +413,8 @@ def bench_ours(args):
         for _ in range(args.steps):
             host_call()
             e2e_sampled += fst.sampled_steps
-        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        e2e_tot = torch.tensor([e2e_sampled], dtype=torch.int64, device=dev)
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=cdev)
+        e2e_tot = torch.tensor([e2e_sampled], dtype=torch.int64, device=cdev)
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
             dist.all_reduce(e2e_tot, op=dist.ReduceOp.SUM)
@@ -433,6 +453,7 @@ def bench_ours(args):
                        "vertices": V, "csr_entries": E_, "queries_per_gpu": n,
                        "replicate_s": None if world == 1 else round(t_rep, 3),
                        "gather_ms": gather_ms,
+                       "backend": backend if world > 1 else None,
                        "parallelism": f"replicated graph, qids partitioned x{world}",
                        "l2": "inputs larger than L2 (graph + result pool > 126 MB), no flush",
                        "sampled_steps_per_gpu_step": sampled // args.steps,

@@ -179,3 +179,36 @@ def test_errors_raise_before_kernel(s16):
                             fw.EngineConfig()))
     with pytest.raises(fw.ConfigError):
         fw.EngineConfig(k_big=1001).validate()
+
+
+def test_torchrun_two_ranks_strong_scaling_gather(tmp_path):
+    """bench.py's multi-rank path end to end: 2 ranks (sharing this box's GPU,
+    gloo for the control collectives), CSR generated on rank 0 and
+    broadcast, qids partitioned (strong scaling), path segments gathered to
+    rank 0 -- the gathered paths must equal one oracle run over all qids."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from paper_2404_08364_b200 import rmat
+    root = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+    out = tmp_path / "gather.npz"
+    n = 6000
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517",
+           os.path.join(root, "bench.py"), "--gpus", "2", "--scale", "14", "--nq", str(n),
+           "--steps", "1", "--warmup", "1", "--scaling", "strong", "--gather",
+           "--dump-gather", str(out), "--no-cpu-baseline", "--no-e2e", "--length", "24"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["queries_per_gpu"] == n // 2
+    z = np.load(out)
+    g = rmat.rmat_graph(14, labels=False)
+    starts = np.arange(n, dtype=np.int64) % g.vertex_count
+    oseq, oln, _ = oracle.walk(g.offsets, g.targets, g.weights, None, starts,
+                               app="node2vec", length=24)
+    np.testing.assert_array_equal(z["lens"], oln)
+    np.testing.assert_array_equal(z["seq"], oseq)

@@ -385,6 +385,10 @@ def bench_ours(args):
         if args.dump_gather and rank == 0:  # consumed by tests/test_gpu_parity.py
             np.savez(args.dump_gather, seq=gathered[0].cpu().numpy().view(np.uint32),
                      lens=gathered[1].cpu().numpy().view(np.uint32))
+    my_ms = sum(launch_ms)
+    st = stats.cpu().numpy()
+    sampled = int(st[6])
+    alg_bytes = int(st[7])
     t = torch.tensor([my_ms], dtype=torch.float64, device=cdev)
     tot = torch.tensor([sampled], dtype=torch.int64, device=cdev)
     if world > 1:

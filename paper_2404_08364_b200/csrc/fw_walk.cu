@@ -492,30 +492,10 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
     const uint32_t off = (uint32_t)(s.elo & 3);
-    // KMODE 2: the draw words of this lane's 4 slots, pre-arranged so one
-    // tile needs two LDS.128 and a per-tile counter offset.  Slot e of lane
-    // p in tile t holds element i = 128t + 4p + e - off, i.e. logical lane
-    // j = i & (k-1) and counter c = i >> log2 k.  For k >= 128 the lane j
-    // repeats with period nph = k/128 tiles and c = t/nph + c0; for k < 128
-    // j is the same every tile and c = t*(128/k) + c0.  Entry (phase, p, e)
-    // stores base(j) + c0*GOLDEN, laid out as [phase][e/2][lane] pairs of u64
-    // so the LDS.128s are bank-conflict free.
-    const uint32_t kshift = 31 - __clz(k);
-    const uint32_t nph = k >= 128 ? k >> 7 : 1;
     if constexpr (KMODE == 2) {
-        ulonglong2 *sw = reinterpret_cast<ulonglong2 *>(fw_smem + woff + kHashSlots);
-        for (uint32_t ph = 0; ph < nph; ph++) {
-            uint64_t wv0[4];
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const int32_t i = (int32_t)(ph * 128 + lane * 4 + e) - (int32_t)off;
-                const uint32_t j = (uint32_t)i & (k - 1);
-                const int64_t c0 = (int64_t)(i >> kshift);  // -1 only for masked slots
-                wv0[e] = lane_base(a, s, j) + (uint64_t)c0 * GOLDEN;
-            }
-            sw[(ph * 2 + 0) * 32 + lane] = make_ulonglong2(wv0[0], wv0[1]);
-            sw[(ph * 2 + 1) * 32 + lane] = make_ulonglong2(wv0[2], wv0[3]);
-        }
+        const uint32_t nl = min(k, deg), kq = k >> 2;
+        uint64_t *sb = reinterpret_cast<uint64_t *>(fw_smem + woff + kHashSlots);
+        for (uint32_t j = lane; j < nl; j += 32) sb[(j & 3) * kq + (j >> 2)] = lane_base(a, s, j);
     }
     const uint32_t *P = a.tgt + s.plo;
     const uint32_t dp = (uint32_t)(s.phi - s.plo);
@@ -595,25 +575,18 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
         carry = __dadd_rn(carry, shfl_d(incl, 31));
         const double pre[4] = {wv[0], p1, p2, p3};
-        uint64_t wds[4];
-        if constexpr (KMODE == 2) {
-            const uint32_t ph = nph > 1 ? (t & (nph - 1)) : 0;
-            const ulonglong2 *sw = reinterpret_cast<const ulonglong2 *>(fw_smem + woff + kHashSlots);
-            const ulonglong2 q0 = sw[(ph * 2 + 0) * 32 + lane];
-            const ulonglong2 q1 = sw[(ph * 2 + 1) * 32 + lane];
-            const uint64_t cadd =
-                (uint64_t)(k >= 128 ? (t >> (kshift - 7)) : (t << (7 - kshift))) * GOLDEN;
-            wds[0] = q0.x + cadd;
-            wds[1] = q0.y + cadd;
-            wds[2] = q1.x + cadd;
-            wds[3] = q1.y + cadd;
-        }
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const uint32_t i = (uint32_t)(i0 + e);
             uint64_t wd;
-            if constexpr (KMODE == 2) wd = wds[e];
-            else wd = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
+            if constexpr (KMODE == 2) {
+                const uint32_t kq = k >> 2;
+                const uint64_t *sb = reinterpret_cast<const uint64_t *>(fw_smem + woff + kHashSlots);
+                wd = sb[((uint32_t)(e - (int)off) & 3u) * kq + ((i >> 2) & (kq - 1))] +
+                     (uint64_t)(i >> (31 - __clz(k))) * GOLDEN;
+            } else {
+                wd = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
+            }
             const double r = u01_word(wd);
             const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
             if (wv[e] > 0.0 && Pr < wv[e]) {

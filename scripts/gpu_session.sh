@@ -1,6 +1,4 @@
 #!/bin/bash
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -25 gpurun_out/pytest_gpu.log | grep -v "^$" | tail -12
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -4 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench_default.json 2>gpurun_out/bench_default.err; echo "bench rc=$?"; cat gpurun_out/bench_default.json
+./scripts/mix_fma_check
+FW_LIB_PATH=$PWD/paper_2404_08364_b200/libflowwalk_fma.so timeout 900 python -m pytest tests -x -q -m gpu -k "golden or s16" > gpurun_out/pytest_fma.log 2>&1; echo "pytest(fma lib) rc=$?"; tail -2 gpurun_out/pytest_fma.log
+bash scripts/gpu_ab.sh paper_2404_08364_b200/libflowwalk_fma.so paper_2404_08364_b200/libflowwalk.so

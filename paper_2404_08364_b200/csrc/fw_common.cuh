@@ -26,30 +26,11 @@ enum { SAMPLER_ZPRS = 0, SAMPLER_DPRS = 1 };
 enum { ST_STEPS = 0, ST_EDGES, ST_COLLECTIVES, ST_DRAWS, ST_SMALL, ST_LARGE, ST_SAMPLED,
        ST_BYTES, ST_COUNT };
 
-#if defined(__CUDA_ARCH__) && defined(FW_MIX_FMA)
-// z ^ (z >> S) with the 64-bit shift done by multiply-high on the FMA pipe
-// (IMAD.HI) instead of funnel shifts on the ALU pipe, which is the binding
-// pipe of the sampler loops.  Bit-identical by construction.
-template <int S>
-__device__ __forceinline__ uint64_t xorshr(uint64_t z) {
-    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
-    const uint32_t m = 1u << (32 - S);
-    const uint32_t nlo = __umulhi(lo, m) + hi * m;  // (lo >> S) | (hi << (32 - S))
-    const uint32_t nhi = __umulhi(hi, m);           // hi >> S
-    return z ^ (((uint64_t)nhi << 32) | nlo);
-}
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-    z = xorshr<30>(z) * MIX1;
-    z = xorshr<27>(z) * MIX2;
-    return xorshr<31>(z);
-}
-#else
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * MIX1;
     z = (z ^ (z >> 27)) * MIX2;
     return z ^ (z >> 31);
 }
-#endif
 
 // u01 from a pre-advanced counter word (base + ctr*GOLDEN).  z>>11 < 2^53 so
 // the int->double conversion and the 2^-53 scaling are both exact.

@@ -156,17 +156,52 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
     if (nl <= 32) {  // one group: physical lane == logical lane
         const uint32_t j = lane;
         double lsum = 0.0;
-        if (j < nl) {
-#pragma unroll 4
-            for (uint32_t i = j; i < deg; i += k) {
-                const double wv = elem_weight<APP>(a, s, i);
-                if (staged) stage[i] = (float)wv;
-                lsum = __dadd_rn(lsum, wv);
-            }
-        }
+        uint32_t cand = 0;
         double ecarry = 0.0;
-        const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
-        const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, staged, woff) : 0;
+        if (APP == APP_METAPATH && staged) {
+            // Most MetaPath weights are 0 (label filter).  A zero weight adds
+            // nothing to the running prefix and can never be accepted, so
+            // lane j keeps only its nonzero elements, compacted in chunk
+            // order into its own staging slots j + k*m (m <= chunk index, so
+            // the list never outruns the dense layout), chunk ids alongside.
+            uint16_t *cst = reinterpret_cast<uint16_t *>(fw_smem + woff + kHashSlots);
+            uint32_t m = 0;
+            if (j < nl) {
+                uint32_t c = 0;
+#pragma unroll 4
+                for (uint32_t i = j; i < deg; i += k, c++) {
+                    const double wv = elem_weight<APP>(a, s, i);
+                    if (wv > 0.0) {
+                        stage[j + k * m] = (float)wv;
+                        cst[j + k * m] = (uint16_t)c;
+                        m++;
+                    }
+                    lsum = __dadd_rn(lsum, wv);
+                }
+            }
+            double run = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
+            if (m) {
+                const uint64_t base = lane_base(a, s, j);
+                for (uint32_t x = 0; x < m; x++) {
+                    const double wv = (double)stage[j + k * x];
+                    const uint32_t c = cst[j + k * x];
+                    run = __dadd_rn(run, wv);
+                    const double r = u01_word(base + (uint64_t)c * GOLDEN);
+                    if (__dmul_rn(r, run) < wv) cand = c * k + j + 1;
+                }
+            }
+        } else {
+            if (j < nl) {
+#pragma unroll 4
+                for (uint32_t i = j; i < deg; i += k) {
+                    const double wv = elem_weight<APP>(a, s, i);
+                    if (staged) stage[i] = (float)wv;
+                    lsum = __dadd_rn(lsum, wv);
+                }
+            }
+            const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
+            cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, staged, woff) : 0;
+        }
         const unsigned m = __ballot_sync(FULL, cand > 0);
         const uint32_t c = __shfl_sync(FULL, cand, m ? 31 - __clz(m) : 0);
         __syncwarp();

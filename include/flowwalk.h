@@ -20,6 +20,9 @@
  *          per-worker stats accumulation (engine.py:342-353).
  *   fw_validate_device
  *       -- _kernels.validate_walks (_kernels.py:486-546).
+ *   fw_sampler_trials_device
+ *       -- the sampler trial kernels seq_rs/dprs/zprs/its/alias/rjs/uniform_control_trials
+ *          (_kernels.py:84-277) behind trials.run_trials (trials.py:46-90).
  *   fw_rmat_edges_device / fw_synth_weights_device / fw_synth_labels_device
  *       -- synthetic inputs; the reference only ships random/star edge lists and
  *          numpy-seeded synthesis (graph.py:172-201, 257-277), see DESIGN.md.
@@ -134,6 +137,15 @@ int fw_validate_device(fw_graph *g, const int64_t *d_starts, uint64_t n,
                        const uint32_t *d_seq, const uint32_t *d_len, uint32_t l_max,
                        const int64_t *schema_host, uint32_t schema_len,
                        int64_t *d_bad, void *stream);
+
+/* Sampler trials (one pick per trial; trial t draws from streams (t<<10)|lane).
+ * method: 0 seq, 1 dprs, 2 zprs, 3 its, 4 alias (d_prob/d_alias = alias table),
+ * 5 rjs (w_max, max_rounds), 6 uniform-control.  d_aux (nullable) receives the
+ * per-trial collectives (dprs/zprs) or rejection rounds (rjs).  All device pointers. */
+int fw_sampler_trials_device(int32_t method, const double *d_w, uint32_t n, uint32_t k,
+                             uint64_t key, uint64_t trials, const double *d_prob,
+                             const int64_t *d_alias, double w_max, uint32_t max_rounds,
+                             uint32_t *d_picks, int64_t *d_aux, void *stream);
 
 /* Synthetic R-MAT (Graph500 a,b,c; d = 1-a-b-c) edges, counter-hash driven so
  * host (numpy) and device generate identical lists.  Writes m (src, dst)

@@ -48,8 +48,8 @@ class FwGraphInfo(ctypes.Structure):
 
 EXPORTS = ("fw_last_error", "fw_device_count", "fw_graph_create", "fw_graph_create_device",
            "fw_graph_destroy", "fw_graph_info_get", "fw_walk", "fw_walk_device",
-           "fw_validate_device", "fw_rmat_edges_device", "fw_synth_weights_device",
-           "fw_synth_labels_device")
+           "fw_validate_device", "fw_sampler_trials_device", "fw_rmat_edges_device",
+           "fw_synth_weights_device", "fw_synth_labels_device")
 
 _lib = None
 
@@ -75,6 +75,7 @@ def load(path=LIB_PATH):
         "fw_walk": ([P, P, U64, U64, P, P, U64, P, P, P], I32),
         "fw_walk_device": ([P, P, U64, U64, P, P, U64, P, P, P, P], I32),
         "fw_validate_device": ([P, P, U64, P, P, U32, P, U32, P, P], I32),
+        "fw_sampler_trials_device": ([I32, P, U32, U32, U64, U64, P, P, D, U32, P, P, P], I32),
         "fw_rmat_edges_device": ([U64, I32, D, D, D, U64, U64, P, P, P], I32),
         "fw_synth_weights_device": ([U64, U64, U64, P, P], I32),
         "fw_synth_labels_device": ([U64, U32, U64, U64, P, P], I32),

@@ -557,6 +557,32 @@ extern "C" int fw_validate_device(fw_graph *g, const int64_t *d_starts, uint64_t
 }
 
 // ---------------------------------------------------------------------------
+// Sampler trials (csrc/fw_trials.cu).
+// ---------------------------------------------------------------------------
+namespace fw {
+cudaError_t launch_trials(int method, const double *w, uint32_t n, uint32_t k, uint64_t key,
+                          uint64_t trials, const double *prob, const int64_t *alias,
+                          double w_max, uint32_t max_rounds, uint32_t *picks, int64_t *aux,
+                          cudaStream_t stream);
+}
+
+extern "C" int fw_sampler_trials_device(int32_t method, const double *d_w, uint32_t n,
+                                        uint32_t k, uint64_t key, uint64_t trials,
+                                        const double *d_prob, const int64_t *d_alias,
+                                        double w_max, uint32_t max_rounds, uint32_t *d_picks,
+                                        int64_t *d_aux, void *stream) {
+    if (method < 0 || method > 6) return set_err(FW_EVALIDATION, "unknown sampler method");
+    if ((method == 1 || method == 2) && (k < 1 || k > 1000))
+        return set_err(FW_ECONFIG, "lane width k must be in [1, 1000]");
+    if (method == 4 && n && (!d_prob || !d_alias))
+        return set_err(FW_EVALIDATION, "alias sampling needs a table");
+    if (trials && !d_picks) return set_err(FW_EVALIDATION, "null picks buffer");
+    CU(launch_trials(method, d_w, n, k, key, trials, d_prob, d_alias, w_max, max_rounds,
+                     d_picks, d_aux, (cudaStream_t)stream));
+    return FW_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Synthetic inputs (counter-hash; paper_2404_08364_b200/rmat.py is the
 // bit-identical numpy twin).
 // ---------------------------------------------------------------------------

@@ -25,6 +25,7 @@ class Golden:
             meta = json.load(fh)
         self.cases = {c["name"]: c for c in meta["cases"]}
         self.kats = meta["kats"]
+        self.trials = meta.get("trials", [])
         self.z = np.load(os.path.join(GOLDEN, "walks.npz"))
 
     def graph(self, name):

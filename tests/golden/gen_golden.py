@@ -134,6 +134,47 @@ def kats():
     return rows
 
 
+def trial_cases():
+    """Sampler trial kernels (_kernels.py:84-277) through trials.run_trials."""
+    from reswalk import _kernels as K
+    from reswalk.samplers import WeightOracle, alias_build
+    rng = np.random.default_rng(77)
+    out, arrays = [], {}
+    vecs = {
+        "u12": rng.uniform(0, 5, 12),
+        "z23": np.where(rng.random(23) < 0.35, 0.0, rng.uniform(0, 5, 23)),
+        "ln300": rng.lognormal(0.0, 1.5, 300),
+        "one": np.array([2.5]),
+        "n1000": rng.uniform(0.1, 4.0, 1000),
+    }
+    for vname, w in vecs.items():
+        arrays[f"t_w_{vname}"] = w
+        tab = alias_build(WeightOracle.from_array(w))
+        arrays[f"t_aliasprob_{vname}"] = tab.prob
+        arrays[f"t_aliasidx_{vname}"] = tab.alias
+        for seed in (3, 2**63 + 11):
+            key = np.uint64(seed)
+            T = 200
+            runs = [("seq", 1, K.seq_rs_trials(w, key, T), None),
+                    ("its", 1, K.its_trials(w, key, T), None),
+                    ("alias", 1, K.alias_trials(tab.prob, tab.alias, key, T), None),
+                    ("uniform-control", 1, K.uniform_control_trials(len(w), key, T), None)]
+            pr, rd = K.rjs_trials(w, float(w.max()), key, T, 10_000)
+            runs.append(("rjs", 1, pr, rd))
+            for k in (1, 3, 32, 256):
+                pd, cd = K.dprs_trials(w, k, key, T)
+                pz, cz = K.zprs_trials(w, k, key, T)
+                runs += [("dprs", k, pd, cd), ("zprs", k, pz, cz)]
+            for sampler, k, picks, aux in runs:
+                name = f"{vname}_{sampler}_{k}_{seed}"
+                arrays[f"t_picks_{name}"] = np.asarray(picks)
+                if aux is not None:
+                    arrays[f"t_aux_{name}"] = np.asarray(aux)
+                out.append(dict(name=name, vec=vname, sampler=sampler, k=k, seed=str(seed),
+                                trials=T))
+    return out, arrays
+
+
 def main():
     gs = graphs()
     arrays = {}
@@ -151,8 +192,10 @@ def main():
         arrays[f"c_{case['name']}_stats"] = st
         arrays[f"c_{case['name']}_starts"] = np.asarray(case.pop("starts"), np.int64)
         print(f"{case['name']:20s} n={len(ln):5d} sampled={int(ln.sum()):7d} stats={st.tolist()}")
+    tcases, tarrays = trial_cases()
+    arrays.update(tarrays)
     np.savez_compressed(os.path.join(OUT, "walks.npz"), **arrays)
-    meta = dict(cases=cs, kats=kats(), generator="tests/golden/gen_golden.py",
+    meta = dict(cases=cs, kats=kats(), trials=tcases, generator="tests/golden/gen_golden.py",
                 reference="reswalk 0.1.0 (/root/reference/pkg), replay mode, workers=2")
     with open(os.path.join(OUT, "cases.json"), "w") as fh:
         json.dump(meta, fh, indent=1)

@@ -212,3 +212,23 @@ def test_torchrun_two_ranks_strong_scaling_gather(tmp_path):
                                app="node2vec", length=24)
     np.testing.assert_array_equal(z["lens"], oln)
     np.testing.assert_array_equal(z["seq"], oseq)
+
+
+def _trial_cases():
+    from conftest import Golden
+    return [c["name"] for c in Golden().trials]
+
+
+@pytest.mark.parametrize("name", _trial_cases())
+def test_sampler_trials_bit_exact(golden, name):
+    """GPU trial kernels == the reference's numba trial kernels
+    (_kernels.py:84-277): picks, collectives per task, rejection rounds."""
+    from paper_2404_08364_b200 import trials
+    case = next(c for c in golden.trials if c["name"] == name)
+    w = golden.z[f"t_w_{case['vec']}"]
+    res = trials.run_trials(case["sampler"], w, case["trials"], int(case["seed"]), k=case["k"])
+    np.testing.assert_array_equal(res.picks, golden.z[f"t_picks_{name}"])
+    key = f"t_aux_{name}"
+    if key in golden.z:
+        aux = res.collectives if res.collectives is not None else res.rounds
+        np.testing.assert_array_equal(aux, golden.z[key])

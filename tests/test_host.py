@@ -120,3 +120,12 @@ def test_perm_bits_is_bijective():
     for s in (1, 5, 10, 16):
         x = np.arange(1 << s, dtype=np.uint64)
         assert len(np.unique(rmat.perm_bits(x, s, 12345))) == 1 << s
+
+
+def test_alias_table_matches_reference(golden):
+    """trials.alias_table restates samplers.alias_build (samplers.py:245-266)."""
+    from paper_2404_08364_b200.trials import alias_table
+    for v in {c["vec"] for c in golden.trials}:
+        prob, alias = alias_table(golden.z[f"t_w_{v}"])
+        np.testing.assert_array_equal(prob, golden.z[f"t_aliasprob_{v}"])
+        np.testing.assert_array_equal(alias, golden.z[f"t_aliasidx_{v}"])

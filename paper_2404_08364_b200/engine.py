@@ -312,15 +312,27 @@ class _Session:
         _lib.load()
         _lib.require_device()
         self.devices = tuple(eng_cfg.devices)
+        self._owned = None
+        self._borrowed = isinstance(g, DeviceGraph)  # the caller's resident graph
         if isinstance(g, DeviceGraph):
             self.handles = [g.handle(d) for d in self.devices]
+        elif len(set(self.devices)) > 1:
+            # one PCIe upload to the first GPU, then device-to-device replica
+            # copies (NVLink peer copies on NVSwitch systems)
+            self._owned = to_device(g, self.devices[0])
+            self.handles = [self._owned.handle(d) for d in self.devices]
         else:
-            with ThreadPoolExecutor(max_workers=len(self.devices)) as ex:
-                self.handles = list(ex.map(lambda d: _upload(g, d), self.devices))
+            h = _upload(g, self.devices[0])
+            self.handles = [h] * len(self.devices)
 
     def close(self):
-        for h in self.handles:
-            h.close()
+        if self._borrowed:
+            return
+        if self._owned is not None:
+            self._owned.close()
+        else:
+            for h in set(self.handles):
+                h.close()
 
 
 def _fw_structs(app_cfg, eng_cfg):

@@ -232,3 +232,16 @@ def test_sampler_trials_bit_exact(golden, name):
     if key in golden.z:
         aux = res.collectives if res.collectives is not None else res.rounds
         np.testing.assert_array_equal(aux, golden.z[key])
+
+
+def test_device_graph_reusable_across_calls(golden):
+    """A resident DeviceGraph survives run() calls (handles are borrowed)."""
+    g = _graph(golden, "rmat12")
+    dg = fw.to_device(g)
+    starts = golden.starts("n2v_rmat12")
+    app = fw.AppConfig(app="node2vec", length=24)
+    for _ in range(2):
+        seq, ln, _st = _run(dg, starts, app, fw.EngineConfig(replay=True), 0)
+        want_seq, want_len, _ = golden.expected("n2v_rmat12")
+        np.testing.assert_array_equal(seq, want_seq)
+        np.testing.assert_array_equal(ln, want_len)

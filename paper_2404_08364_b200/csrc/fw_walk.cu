@@ -61,9 +61,11 @@ template <int APP>
 __device__ __forceinline__ double elem_weight(const WalkArgs &a, const StepCtx &s, uint32_t i) {
     const int64_t e = s.elo + i;
     if constexpr (APP == APP_METAPATH) {
+        // both loads issued up front (a dependent weight load would cost a
+        // second memory round trip per element)
         const int64_t lab = a.lab ? (int64_t)ldg(a.lab + e) : 0;
-        if (lab != s.want) return 0.0;
-        return a.weighted ? (double)ldg(a.w + e) : 1.0;
+        const float w = a.weighted ? ldg(a.w + e) : 1.0f;
+        return lab == s.want ? (double)w : 0.0;
     } else if constexpr (APP == APP_NODE2VEC) {
         if (s.prev >= 0) {
             const uint32_t u = ldg(a.tgt + e);
@@ -76,6 +78,25 @@ __device__ __forceinline__ double elem_weight(const WalkArgs &a, const StepCtx &
     } else {
         return a.weighted ? (double)ldg(a.w + e) : 1.0;
     }
+}
+
+// First-order apps (DeepWalk/PPR/MetaPath): the app weights of elements
+// i, i+k, i+2k, i+3k with all loads issued before any is used (the ZPRS
+// lane loops are latency-bound otherwise).
+template <int APP>
+__device__ __forceinline__ void weights4(const WalkArgs &a, const StepCtx &s, uint32_t i,
+                                         uint32_t k, double x[4]) {
+    float w[4];
+    int lab[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const int64_t e = s.elo + i + (uint32_t)r * k;
+        w[r] = a.weighted ? ldg(a.w + e) : 1.0f;
+        lab[r] = (APP == APP_METAPATH && a.lab) ? (int)ldg(a.lab + e) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+        x[r] = (APP != APP_METAPATH || (int64_t)lab[r] == s.want) ? (double)w[r] : 0.0;
 }
 
 __device__ __forceinline__ uint64_t lane_base(const WalkArgs &a, const StepCtx &s, uint32_t j) {
@@ -134,8 +155,20 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
             if (wv > 0.0 && __dmul_rn(r, run) < wv) cand = i + 1;
         }
     } else {
-#pragma unroll 4
-        for (uint32_t i = j; i < deg; i += k, word += GOLDEN) {
+        uint32_t i = j;
+        if constexpr (APP != APP_NODE2VEC) {
+            for (; i + 3 * k < deg; i += 4 * k) {
+                double x[4];
+                weights4<APP>(a, s, i, k, x);
+#pragma unroll
+                for (int r = 0; r < 4; r++, word += GOLDEN) {
+                    run = __dadd_rn(run, x[r]);
+                    const double u = u01_word(word);
+                    if (x[r] > 0.0 && __dmul_rn(u, run) < x[r]) cand = i + r * k + 1;
+                }
+            }
+        }
+        for (; i < deg; i += k, word += GOLDEN) {
             const double wv = elem_weight<APP>(a, s, i);
             run = __dadd_rn(run, wv);
             const double r = u01_word(word);
@@ -143,6 +176,34 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
         }
     }
     return cand;
+}
+
+// Pass 1 of ZPRS for logical lane j: the lane sum in chunk order (the
+// reference's order), optionally staging the weights at their element index.
+template <int APP>
+__device__ __forceinline__ double zprs_lane_pass1(const WalkArgs &a, const StepCtx &s,
+                                                  uint32_t j, uint32_t k, bool staged,
+                                                  float *stage) {
+    double lsum = 0.0;
+    const uint32_t deg = s.deg;
+    uint32_t i = j;
+    if constexpr (APP != APP_NODE2VEC) {
+        for (; i + 3 * k < deg; i += 4 * k) {
+            double x[4];
+            weights4<APP>(a, s, i, k, x);
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                if (staged) stage[i + r * k] = (float)x[r];
+                lsum = __dadd_rn(lsum, x[r]);
+            }
+        }
+    }
+    for (; i < deg; i += k) {
+        const double wv = elem_weight<APP>(a, s, i);
+        if (staged) stage[i] = (float)wv;
+        lsum = __dadd_rn(lsum, wv);
+    }
+    return lsum;
 }
 
 template <int APP, bool EXACT>
@@ -167,9 +228,21 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
             uint16_t *cst = reinterpret_cast<uint16_t *>(fw_smem + woff + kHashSlots);
             uint32_t m = 0;
             if (j < nl) {
-                uint32_t c = 0;
-#pragma unroll 4
-                for (uint32_t i = j; i < deg; i += k, c++) {
+                uint32_t c = 0, i = j;
+                for (; i + 3 * k < deg; i += 4 * k) {
+                    double x[4];
+                    weights4<APP>(a, s, i, k, x);
+#pragma unroll
+                    for (int r = 0; r < 4; r++, c++) {
+                        if (x[r] > 0.0) {
+                            stage[j + k * m] = (float)x[r];
+                            cst[j + k * m] = (uint16_t)c;
+                            m++;
+                        }
+                        lsum = __dadd_rn(lsum, x[r]);
+                    }
+                }
+                for (; i < deg; i += k, c++) {
                     const double wv = elem_weight<APP>(a, s, i);
                     if (wv > 0.0) {
                         stage[j + k * m] = (float)wv;
@@ -191,14 +264,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
                 }
             }
         } else {
-            if (j < nl) {
-#pragma unroll 4
-                for (uint32_t i = j; i < deg; i += k) {
-                    const double wv = elem_weight<APP>(a, s, i);
-                    if (staged) stage[i] = (float)wv;
-                    lsum = __dadd_rn(lsum, wv);
-                }
-            }
+            if (j < nl) lsum = zprs_lane_pass1<APP>(a, s, j, k, staged, stage);
             const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
             cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, staged, woff) : 0;
         }
@@ -213,15 +279,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
         double ecarry = 0.0;
         for (uint32_t g = 0; g < ng; g++) {
             const uint32_t j = g * 32 + lane;
-            double lsum = 0.0;
-            if (j < nl) {
-#pragma unroll 4
-                for (uint32_t i = j; i < deg; i += k) {
-                    const double wv = elem_weight<APP>(a, s, i);
-                    if (staged) stage[i] = (float)wv;
-                    lsum = __dadd_rn(lsum, wv);
-                }
-            }
+            const double lsum = j < nl ? zprs_lane_pass1<APP>(a, s, j, k, staged, stage) : 0.0;
             E[j] = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
         }
         __syncwarp();
@@ -243,11 +301,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
     uint32_t best = 0;
     for (uint32_t g0 = 0; g0 < nl; g0 += 32) {
         const uint32_t j = g0 + lane;
-        double lsum = 0.0;
-        if (j < nl) {
-#pragma unroll 4
-            for (uint32_t i = j; i < deg; i += k) lsum = __dadd_rn(lsum, elem_weight<APP>(a, s, i));
-        }
+        const double lsum = j < nl ? zprs_lane_pass1<APP>(a, s, j, k, false, nullptr) : 0.0;
         const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
         const uint32_t cand = j < nl ? zprs_lane_pass2<APP>(a, s, j, k, excl, false, woff) : 0;
         const unsigned m = __ballot_sync(FULL, cand > 0);

@@ -589,6 +589,13 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
     const uint32_t *P = a.tgt + s.plo;
     const uint32_t dp = (uint32_t)(s.phi - s.plo);
     const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
+    // tile 0's targets are requested before the table build so the two
+    // memory round trips of a step's prologue overlap
+    const uint32_t span = deg + off;
+    const uint32_t ntiles = (span + 127) >> 7;
+    const int64_t ebase = s.elo - off;
+    uint4 nu = make_uint4(0, 0, 0, 0);
+    if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + lane);
     uint32_t lim = 0, hshift = 0;
     if (use_hash) {
         const HashState hs = hash_build(P, 0, dp, woff, lane);
@@ -597,11 +604,6 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
     } else {
         __syncwarp();
     }
-    const uint32_t span = deg + off;
-    const uint32_t ntiles = (span + 127) >> 7;
-    const int64_t ebase = s.elo - off;
-    uint4 nu = make_uint4(0, 0, 0, 0);
-    if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + lane);
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
     for (uint32_t t = 0; t < ntiles; t++) {

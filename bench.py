@@ -346,11 +346,12 @@ def bench_ours(args):
     L = app.length
     seq = torch.empty(n * L, dtype=torch.int32, device=dev)
     lens = torch.empty(n, dtype=torch.int32, device=dev)
-    stats = torch.zeros(8, dtype=torch.int64, device=dev)
+    stats = torch.zeros(10, dtype=torch.int64, device=dev)
     a_s, e_s, _schema = _fw_structs(app, fw.EngineConfig(replay=True))
     stream = torch.cuda.current_stream(dev)
 
     def launch():
+        stats[8:].zero_()  # per-launch first/last warp exit words
         _lib.check(lib.fw_walk_device(handle, starts.data_ptr(), n, base_qid, ctypes.byref(a_s),
                                       ctypes.byref(e_s), 0, seq.data_ptr(), lens.data_ptr(),
                                       stats.data_ptr(), stream.cuda_stream))
@@ -387,6 +388,9 @@ def bench_ours(args):
                      lens=gathered[1].cpu().numpy().view(np.uint32))
     my_ms = sum(launch_ms)
     st = stats.cpu().numpy()
+    tail = {"last_launch_ms": launch_ms[-1],
+            "tail_ms": (int(st[8]) - int(~np.uint64(st[9].view(np.uint64)))) * 1e-6,
+            "note": "first to last warp exit in the last timed launch (%globaltimer)"}
     sampled = int(st[6])
     alg_bytes = int(st[7])
     t = torch.tensor([my_ms], dtype=torch.float64, device=cdev)
@@ -463,7 +467,7 @@ def bench_ours(args):
                        "sampled_steps_per_gpu_step": sampled // args.steps,
                        "walk_attempts_per_step": int(st[0]) // args.steps},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps, "load_imbalance_tail": tail,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

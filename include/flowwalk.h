@@ -92,6 +92,7 @@ typedef struct {
     int32_t grid_ctas;
     int32_t kernel_launches;
     int32_t reserved;
+    double tail_ms;         /* first to last warp exit: the load-imbalance tail */
 } fw_stats;
 
 typedef struct {
@@ -125,8 +126,9 @@ int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t base_qid,
             uint32_t *out_seq, uint32_t *out_len, fw_stats *stats);
 
 /* Device-buffer walk, asynchronous on `stream` (a cudaStream_t, may be NULL).
- * d_stats (int64[8], device) is ACCUMULATED: steps, edges, collectives, draws,
- * small, large, sampled_steps, alg_bytes. */
+ * d_stats (int64[10], device) is ACCUMULATED: steps, edges, collectives, draws,
+ * small, large, sampled_steps, alg_bytes; words 8/9 take the max of the warps'
+ * exit time and of its complement (%globaltimer ns, zero them per launch). */
 int fw_walk_device(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t base_qid,
                    const fw_app *app, const fw_engine *eng, uint64_t seed,
                    uint32_t *d_out_seq, uint32_t *d_out_len, int64_t *d_stats,

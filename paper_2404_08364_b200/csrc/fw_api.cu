@@ -433,7 +433,7 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     CU(g->starts.reserve(std::max<uint64_t>(n, 1) * sizeof(int64_t)));
     CU(g->seq.reserve(std::max<uint64_t>(n * L, 1) * sizeof(uint32_t)));
     CU(g->len.reserve(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
-    CU(g->stats.reserve(ST_COUNT * sizeof(int64_t)));
+    CU(g->stats.reserve(ST_WORDS * sizeof(int64_t)));
     cudaStream_t st;
     CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     cudaEvent_t e0, e1, e2, e3;
@@ -442,7 +442,7 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     cudaEventCreate(&e2);
     cudaEventCreate(&e3);
     cudaEventRecord(e0, st);
-    cudaMemsetAsync(g->stats.p, 0, ST_COUNT * sizeof(int64_t), st);
+    cudaMemsetAsync(g->stats.p, 0, ST_WORDS * sizeof(int64_t), st);
     if (n) cudaMemcpyAsync(g->starts.p, starts, n * sizeof(int64_t), cudaMemcpyHostToDevice, st);
     cudaEventRecord(e1, st);
     bool exact = false;
@@ -451,7 +451,7 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
                 (uint32_t *)g->seq.p, (uint32_t *)g->len.p, (int64_t *)g->stats.p, st, &exact,
                 &grid);
     cudaEventRecord(e2, st);
-    int64_t hst[ST_COUNT] = {0};
+    int64_t hst[ST_WORDS] = {0};
     if (!rc) {
         if (n) {
             cudaMemcpyAsync(out_seq, g->seq.p, n * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
@@ -480,6 +480,8 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         stats->exact_order = exact;
         stats->grid_ctas = grid;
         stats->kernel_launches = n ? 1 : 0;
+        const uint64_t last = (uint64_t)hst[ST_T_LAST], first = ~(uint64_t)hst[ST_T_FIRST_NEG];
+        stats->tail_ms = (n && last >= first) ? (double)(last - first) * 1e-6 : 0.0;
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

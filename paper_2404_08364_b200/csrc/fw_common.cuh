@@ -25,6 +25,9 @@ enum { APP_DEEPWALK = 0, APP_PPR = 1, APP_NODE2VEC = 2, APP_METAPATH = 3 };
 enum { SAMPLER_ZPRS = 0, SAMPLER_DPRS = 1 };
 enum { ST_STEPS = 0, ST_EDGES, ST_COLLECTIVES, ST_DRAWS, ST_SMALL, ST_LARGE, ST_SAMPLED,
        ST_BYTES, ST_COUNT };
+// extra device words after the counters: max over warps of the exit time and
+// of its complement (%globaltimer ns) -> first/last warp exit of a launch
+enum { ST_T_LAST = ST_COUNT, ST_T_FIRST_NEG, ST_WORDS };
 
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * MIX1;

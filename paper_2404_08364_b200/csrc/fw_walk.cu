@@ -840,6 +840,10 @@ walk_kernel(const WalkArgs a) {
 #pragma unroll
         for (int i = 0; i < ST_COUNT; i++)
             if (st[i]) atomicAdd((unsigned long long *)(a.stats + i), st[i]);
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        atomicMax((unsigned long long *)(a.stats + ST_T_LAST), now);
+        atomicMax((unsigned long long *)(a.stats + ST_T_FIRST_NEG), ~now);
     }
 }
 

@@ -107,7 +107,7 @@ def test_device_graph_walk_and_validator():
     L = 40
     seq = torch.empty(n * L, dtype=torch.int32, device="cuda")
     ln = torch.empty(n, dtype=torch.int32, device="cuda")
-    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(10, dtype=torch.int64, device="cuda")
     app = fw.AppConfig(app="node2vec", length=L)
     eng = fw.EngineConfig()
     from paper_2404_08364_b200.engine import _fw_structs

@@ -245,3 +245,81 @@ def test_device_graph_reusable_across_calls(golden):
         want_seq, want_len, _ = golden.expected("n2v_rmat12")
         np.testing.assert_array_equal(seq, want_seq)
         np.testing.assert_array_equal(ln, want_len)
+
+
+def _chi2_pass(counts, probs, alpha=1e-3):
+    """Pearson chi-square with bins of expected count < 5 pooled."""
+    from scipy.stats import chi2
+    n = counts.sum()
+    exp = probs * n
+    order = np.argsort(exp)
+    obs_p, exp_p, acc_o, acc_e = [], [], 0.0, 0.0
+    for i in order:
+        acc_o += counts[i]
+        acc_e += exp[i]
+        if acc_e >= 5:
+            obs_p.append(acc_o)
+            exp_p.append(acc_e)
+            acc_o = acc_e = 0.0
+    if acc_e > 0 and exp_p:
+        obs_p[-1] += acc_o
+        exp_p[-1] += acc_e
+    obs_p, exp_p = np.array(obs_p), np.array(exp_p)
+    stat = float(((obs_p - exp_p) ** 2 / exp_p).sum())
+    dof = max(len(exp_p) - 1, 1)
+    return stat <= chi2.ppf(1 - alpha, dof), stat, dof
+
+
+def test_node2vec_second_order_distribution_chi_square():
+    """North-star statistical gate: the GPU's second-order Node2Vec
+    transitions follow the exact fp64 probabilities (the reference's
+    node2vec_bruteforce, stats.py:142-164, restated here)."""
+    g = rmat.rmat_graph(12)
+    deg = np.diff(g.offsets)
+    s0 = int(np.argsort(deg)[-40])            # a mid-size hub as the start
+    n = 400_000
+    app = fw.AppConfig(app="node2vec", length=2, a=2.0, b=0.5)
+    seq, ln, _ = _run(g, np.full(n, s0, np.int64), app, fw.EngineConfig(replay=True), 123)
+    ok = ln == 2
+    first, second = seq[ok, 0].astype(np.int64), seq[ok, 1].astype(np.int64)
+    checked = 0
+    for v in np.unique(first):
+        sel = first == v
+        if sel.sum() < 20_000:
+            continue
+        lo, hi = int(g.offsets[v]), int(g.offsets[v + 1])
+        prev_set = set(g.targets[g.offsets[s0]:g.offsets[s0 + 1]].tolist())
+        w = []
+        for e in range(lo, hi):
+            u = int(g.targets[e])
+            base = 0.5 if u == s0 else (1.0 if u in prev_set else 2.0)
+            w.append(base * float(g.weights[e]))
+        w = np.array(w)
+        probs = w / w.sum()
+        # picks are targets; map them to edge slots (duplicates share mass)
+        tg = g.targets[lo:hi].astype(np.int64)
+        uniq, inv = np.unique(tg, return_inverse=True)
+        p_u = np.bincount(inv, weights=probs, minlength=len(uniq))
+        idx = np.searchsorted(uniq, second[sel])
+        counts = np.bincount(idx, minlength=len(uniq)).astype(np.float64)
+        passed, stat, dof = _chi2_pass(counts, p_u)
+        assert passed, (int(v), stat, dof)
+        checked += 1
+    assert checked >= 3
+
+
+def test_deepwalk_one_step_distribution_chi_square():
+    g = rmat.rmat_graph(12)
+    s0 = int(np.argmax(np.diff(g.offsets)))
+    n = 300_000
+    seq, ln, _ = _run(g, np.full(n, s0, np.int64), fw.AppConfig(app="deepwalk", length=1),
+                      fw.EngineConfig(replay=True), 7)
+    lo, hi = int(g.offsets[s0]), int(g.offsets[s0 + 1])
+    w = g.weights[lo:hi].astype(np.float64)
+    tg = g.targets[lo:hi].astype(np.int64)
+    uniq, inv = np.unique(tg, return_inverse=True)
+    p_u = np.bincount(inv, weights=w / w.sum(), minlength=len(uniq))
+    counts = np.bincount(np.searchsorted(uniq, seq[:, 0].astype(np.int64)),
+                         minlength=len(uniq)).astype(np.float64)
+    passed, stat, dof = _chi2_pass(counts, p_u)
+    assert passed, (stat, dof)

@@ -283,9 +283,10 @@ def test_node2vec_second_order_distribution_chi_square():
     ok = ln == 2
     first, second = seq[ok, 0].astype(np.int64), seq[ok, 1].astype(np.int64)
     checked = 0
-    for v in np.unique(first):
+    vs, cnt = np.unique(first, return_counts=True)
+    for v in vs[np.argsort(cnt)[::-1][:6]]:   # the six most visited first hops
         sel = first == v
-        if sel.sum() < 20_000:
+        if sel.sum() < 3_000:
             continue
         lo, hi = int(g.offsets[v]), int(g.offsets[v + 1])
         prev_set = set(g.targets[g.offsets[s0]:g.offsets[s0 + 1]].tolist())

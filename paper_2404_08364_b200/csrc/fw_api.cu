@@ -376,6 +376,14 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     a.fac[1] = 1.0;
     a.fac[2] = app->inv_a;
     a.fac[3] = app->inv_a;
+    {   // largest app weight, rounded up to fp32 (node2vec accept prefilter)
+        double fmax = 1.0;
+        if (app->app_id == FW_APP_NODE2VEC) fmax = std::max({1.0, app->inv_a, app->inv_b});
+        const double wm = fmax * (app->weighted ? (double)g->info.max_weight : 1.0);
+        float f = (float)wm;
+        if ((double)f < wm) f = std::nextafter(f, INFINITY);
+        a.accept_wmax = (std::isfinite(f) && f <= 1e37f) ? f : INFINITY;  // inf: prefilter off
+    }
     a.k_small = eng->k_small;
     a.k_big = eng->k_big;
     a.d_t = eng->d_t;

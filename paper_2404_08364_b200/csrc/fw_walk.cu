@@ -15,6 +15,7 @@
 // (32 logical lanes per warp pass) is free, so results are bit-identical
 // for any k in [1, 1000].
 #include <cuda_runtime.h>
+#include <climits>
 #include <cstdint>
 
 #include "fw_common.cuh"
@@ -25,6 +26,10 @@ namespace fw {
 // Cold helpers (window advance, hash build, binary-search fallback).
 // Inlined by default: an out-of-line call makes the tile loop save and
 // restore registers around it (measured 6.3e7 vs 5.4e7 steps/s).
+#ifndef FW_PREFILTER
+#define FW_PREFILTER 0
+#endif
+
 #ifdef FW_COLD_OUTLINE
 #define FW_COLD __noinline__
 #else
@@ -425,16 +430,30 @@ __device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
     return scan_round<16>(v, lane);
 }
 
-// Bucketed open addressing in the warp's shared-memory slice: 4 slots (16
-// bytes) per bucket, filled in slot order, buckets probed linearly.  A
-// lookup is one LDS.128; it continues to the next bucket only when the
-// bucket is full and the key is absent (rare at load <= 1/4), so a warp
-// rarely waits on its slowest lane.  The window over N(prev) is described
-// by two registers in the hot loop (lim = max key of the chunk, or ~0 for
-// the last chunk; hshift = 32 - log2 #buckets); the rest (chunk start and
-// length, d(prev)) sits in the warp's control words (kCtlWord).
-__device__ __forceinline__ uint32_t hbucket(uint32_t u, uint32_t shift) {
-    return (u * 0x9E3779B1u) >> shift;
+// Membership table for a window of N(prev): an order-preserving hashed
+// sorted array in the warp's shared-memory slice, built without atomics.
+// A chunk of cn <= kChunk sorted keys k_0..k_{cn-1} (min kmin, max kmax) is
+// mapped to kGroups groups of 4 slots by the monotone bucket function
+//   b(u) = min(umulhi(u - kmin, scale), kGroups - 1),
+//   scale ~ kGroups * 2^32 / (kmax - kmin + 1),
+// and key i goes to slot pos_i = i + max_{j<=i}(4 b_j - j): the first free
+// slot at or after its group start, keeping the table sorted (a warp
+// max-scan, no atomics, no collisions).  pos_i <= 4(kGroups-1) + cn - 1 <
+// kHashSlots.  A lookup reads group b(u) with one LDS.128; u is present iff
+// it is in that group, or -- when the group is full and its last key is < u
+// (rare) -- in a following group.  Empty slots hold kEmpty (> any vertex
+// id).  The window over N(prev) is described by three registers in the hot
+// loop (kmin, scale, lim = kmax or ~0 for the last chunk); chunk start,
+// length and d(prev) sit in the warp's control words (kCtlWord).
+constexpr uint32_t kGroups = 192;
+static_assert(4 * (kGroups - 1) + kChunk <= kHashSlots, "table overflow");
+
+struct HashState {
+    uint32_t kmin, scale, lim;
+};
+
+__device__ __forceinline__ uint32_t tab_group(uint32_t u, const HashState &hs) {
+    return min(__umulhi(u - hs.kmin, hs.scale), kGroups - 1);
 }
 __device__ __forceinline__ uint4 bucket_at(uint32_t woff, uint32_t b) {
     return reinterpret_cast<const uint4 *>(fw_smem + woff)[b];
@@ -443,31 +462,13 @@ __device__ __forceinline__ bool bucket_has(const uint4 q, uint32_t u) {
     return q.x == u || q.y == u || q.z == u || q.w == u;
 }
 
-// Build the table from P[c0, c0 + min(kChunk, dp - c0)); returns hshift
-// and sets lim.  Control words: [0] = c0, [1] = cn, [2] = dp.
-struct HashState {
-    uint32_t hshift, lim;
-};
-
+// Build the table from P[c0, c0 + min(kChunk, dp - c0)).  Control words:
+// [0] = c0, [1] = cn, [2] = dp.
 __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t c0,
-                                             uint32_t dp, uint32_t woff, int lane) {
+                                        uint32_t dp, uint32_t woff, int lane) {
     const uint32_t cn = min(kChunk, dp - c0);
-    uint32_t bits = 3;
-    while ((1u << bits) < cn) bits++;  // >= cn buckets: load <= 1/4
-    const uint32_t nb = 1u << bits;
-    const uint32_t shift = 32 - bits;
-    __syncwarp();
-    uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + woff);
-    for (uint32_t x = lane; x < nb; x += 32) t4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    if (lane == 0) {
-        fw_smem[woff + kCtlWord + 0] = c0;
-        fw_smem[woff + kCtlWord + 1] = cn;
-        fw_smem[woff + kCtlWord + 2] = dp;
-    }
-    __syncwarp();
     const uint32_t *src = P + c0;
-    // all of this lane's keys are requested before the first insert (the
-    // loads are independent; inserting as they arrive serialised them)
+    // all of this lane's keys are requested first (independent loads)
     constexpr int kKeys = kChunk / 32;
     uint32_t keys[kKeys];
 #pragma unroll
@@ -475,55 +476,64 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t
         const uint32_t x = r * 32 + lane;
         keys[r] = x < cn ? ldg(src + x) : kEmpty;
     }
+    const uint32_t kmax = ldg(src + cn - 1);
+    __syncwarp();  // previous readers of the table are done
+    uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + woff);
 #pragma unroll
-    for (int r = 0; r < kKeys; r++) {
-        const uint32_t key = keys[r];
-        if (key == kEmpty) continue;
-        uint32_t b = hbucket(key, shift);
-        for (;;) {
-            uint32_t old = kEmpty;
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                old = atomicCAS(fw_smem + woff + b * 4 + q, kEmpty, key);
-                if (old == kEmpty || old == key) break;
-            }
-            if (old == kEmpty || old == key) break;
-            b = (b + 1) & (nb - 1);
-        }
+    for (int x = 0; x < (int)(kHashSlots / 128); x++)
+        t4[x * 32 + lane] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    if (lane == 0) {
+        fw_smem[woff + kCtlWord + 0] = c0;
+        fw_smem[woff + kCtlWord + 1] = cn;
+        fw_smem[woff + kCtlWord + 2] = dp;
     }
     HashState hs;
-    hs.lim = c0 + cn >= dp ? kEmpty : ldg(src + cn - 1);
-    hs.hshift = shift;
+    hs.kmin = __shfl_sync(FULL, keys[0], 0);
+    const float range = (float)(kmax - hs.kmin) + 1.0f;
+    hs.scale = (uint32_t)fminf((float)kGroups * 4294967296.0f / range, 4294967040.0f);
+    hs.lim = c0 + cn >= dp ? kEmpty : kmax;
+    __syncwarp();
+    int carry = INT_MIN;
+#pragma unroll
+    for (int r = 0; r < kKeys; r++) {
+        const int i = r * 32 + lane;
+        const bool valid = (uint32_t)i < cn;
+        int v = valid ? (int)(4 * tab_group(keys[r], hs)) - i : INT_MIN;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) v = max(v, __shfl_up_sync(FULL, v, d));  // idempotent
+        v = max(v, carry);
+        carry = __shfl_sync(FULL, v, 31);
+        if (valid) fw_smem[woff + i + v] = keys[r];
+    }
     __syncwarp();
     return hs;
 }
 
-// Lookups whose first bucket was full, and the window advance (cold path).
+// Continuation probes (a full group whose last key is < u) and the window
+// advance (cold path).
 struct SlowRet {
-    uint32_t mem, hshift, lim;
+    uint32_t mem;
+    HashState hs;
 };
 
 __device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ P, uint32_t woff,
-                                             uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3,
-                                             uint32_t full, uint32_t need, uint32_t hshift,
-                                             uint32_t lim, int lane) {
+                                        uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3,
+                                        uint32_t full, uint32_t need, HashState hs, int lane) {
     const uint32_t u[4] = {u0, u1, u2, u3};
     uint32_t mem = 0;
     for (;;) {
-        const uint32_t bmask = (1u << (32 - hshift)) - 1;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             if ((full >> e) & 1) {
-                uint32_t b = hbucket(u[e], hshift);
+                uint32_t g = tab_group(u[e], hs);
                 for (;;) {
-                    b = (b + 1) & bmask;
-                    const uint4 q = bucket_at(woff, b);
+                    const uint4 q = bucket_at(woff, ++g);
                     if (bucket_has(q, u[e])) { mem |= 1u << e; break; }
-                    if (q.w == kEmpty) break;
+                    if (!(q.w < u[e])) break;
                 }
             }
         }
-        if (!__any_sync(FULL, need)) return SlowRet{mem, hshift, lim};
+        if (!__any_sync(FULL, need)) return SlowRet{mem, hs};
         uint32_t umin = kEmpty;
 #pragma unroll
         for (int e = 3; e >= 0; e--)
@@ -533,18 +543,16 @@ __device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ P, uint32_t
         const uint32_t dp = fw_smem[woff + kCtlWord + 2];
         uint32_t c0 = fw_smem[woff + kCtlWord + 0] + fw_smem[woff + kCtlWord + 1];
         while (c0 + kChunk < dp && ldg(P + c0 + kChunk - 1) < umin) c0 += kChunk;
-        const HashState hs = hash_build(P, c0, dp, woff, lane);
-        hshift = hs.hshift;
-        lim = hs.lim;
+        hs = hash_build(P, c0, dp, woff, lane);
         full = 0;
         uint32_t here = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            if (((need >> e) & 1) && u[e] <= lim) {
+            if (((need >> e) & 1) && u[e] <= hs.lim) {
                 here |= 1u << e;
-                const uint4 q = bucket_at(woff, hbucket(u[e], hshift));
+                const uint4 q = bucket_at(woff, tab_group(u[e], hs));
                 if (bucket_has(q, u[e])) mem |= 1u << e;
-                else if (q.w != kEmpty) full |= 1u << e;
+                else if (q.w < u[e]) full |= 1u << e;
             }
         }
         need &= ~here;
@@ -571,39 +579,227 @@ __device__ FW_COLD uint32_t member4_bsearch(const uint32_t *__restrict__ P, uint
     return mem;
 }
 
-// KMODE 2: power-of-two 4 <= k <= 256: lane bases staged in shared memory,
-//          bank-conflict-free layout (j & 3) * k/4 + j/4 (slot e of lane p
-//          reads row (e-off)&3, column (32t+p+..) & (k/4-1));
-// KMODE 0: any other k (bases recomputed per element).
+// High word of the second multiply of mix64 (the final xorshift flips at
+// most bit 0 of it).
+__device__ __forceinline__ uint32_t mix64_yhi(uint64_t z) {
+    z = (z ^ (z >> 30)) * MIX1;
+    z = z ^ (z >> 27);
+    return (uint32_t)((z * MIX2) >> 32);
+}
+
+// Prefilter threshold for a lane whose elements all have prefix P >= base + w:
+// >= floor(T * 2^32) + 2 with T = wmax / (base + wmax), saturated.  The fp32
+// estimate of T (conversion, add, approximate divide) is within 2^-20
+// relative; the 2^-12 margin covers it.  base beyond the fp32 range gives
+// t = 0 and thr = 2, still >= floor(T * 2^32) + 2 = 2.
+__device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
+    const float b = (float)base;
+    const float t = __fdividef(wmax, b + wmax);
+    const uint32_t thr = __float2uint_rz(fmaf(t, 4294967296.0f * 1.000244140625f, 2.0f));
+    return wmax <= 1e37f ? thr : 0xFFFFFFFFu;  // the host passes +inf to disable
+}
+
+// 64-bit warp shuffle from an arbitrary source lane.
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t x, int src) {
+    const uint32_t lo = __shfl_sync(FULL, (uint32_t)x, src);
+    const uint32_t hi = __shfl_sync(FULL, (uint32_t)(x >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// Per-lane draw words for power-of-two k (4 <= k <= 256).  Element i of
+// tile t is i = 128t + s_e with s_e = 4*lane + e - off in [-3, 127]:
+//   k <= 128: lane i mod k = s_e mod k and counter i div k = t*128/k +
+//             (s_e >> log2 k), so word_e(t) = W_e + t*(128/k)*GOLDEN;
+//   k == 256: lane (128*(t&1) + s_e) mod 256 and counter (t>>1) +
+//             ((128*(t&1) + s_e) >> 8), so word_e(t) = W_e[t&1] + (t>>1)*GOLDEN.
+// W is stored lane-private as [tau][e>>1][lane][e&1] (u64), read with two
+// conflict-free LDS.128 per tile.
+__device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s, uint32_t k,
+                                            int lane, uint32_t woff, uint32_t off) {
+    uint64_t *W = reinterpret_cast<uint64_t *>(fw_smem + woff + kHashSlots);
+    const uint32_t lk = 31 - __clz(k);
+    if (k <= 32) {
+        const uint64_t b = (uint32_t)lane < k ? lane_base(a, s, lane) : 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const int sidx = 4 * lane + e - (int)off;
+            const uint64_t bj = shfl_u64(b, sidx & (int)(k - 1));
+            W[((e >> 1) * 32 + lane) * 2 + (e & 1)] =
+                bj + (uint64_t)(int64_t)(sidx >> lk) * GOLDEN;
+        }
+    } else {
+        const int ntau = k == 256 ? 2 : 1;
+        for (int tau = 0; tau < ntau; tau++) {
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int sidx = 4 * lane + e - (int)off + 128 * tau;
+                W[((tau * 2 + (e >> 1)) * 32 + lane) * 2 + (e & 1)] =
+                    lane_base(a, s, (uint32_t)sidx & (k - 1)) +
+                    (uint64_t)(int64_t)(sidx >> lk) * GOLDEN;
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// Node2Vec DPRS, exact order, prev >= 0, power-of-two 4 <= k <= 256 (the
+// headline path).  Per 128-element tile: 16-byte loads of targets (one tile
+// ahead) and weights, branch-free membership lookups into the N(prev) table,
+// a 4-element local prefix plus one warp scan, draw words from the staged
+// per-lane table, and the accept test.
+__device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
+                                  uint32_t woff, uint32_t &sel_u) {
+    const uint32_t deg = s.deg;
+    const uint32_t prev = (uint32_t)s.prev;
+    const uint32_t off = (uint32_t)(s.elo & 3);
+    const uint32_t *P = a.tgt + s.plo;
+    const uint32_t dp = (uint32_t)(s.phi - s.plo);
+    const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
+    const uint32_t span = deg + off;
+    const uint32_t ntiles = (span + 127) >> 7;
+    const int64_t ebase = s.elo - off;
+    const uint4 *T4 = reinterpret_cast<const uint4 *>(a.tgt + ebase);
+    const float4 *W4 = reinterpret_cast<const float4 *>(a.w + ebase);
+    // tile 0's targets are requested before the table build so the memory
+    // round trips of a step's prologue overlap
+    uint4 nu = make_uint4(0, 0, 0, 0);
+    if ((uint32_t)lane * 4 < span) nu = ldg(T4 + lane);
+    stage_words(a, s, k, lane, woff, off);
+    HashState hs{0, 0, 0};
+    if (use_hash) hs = hash_build(P, 0, dp, woff, lane);
+    const uint64_t *Wst = reinterpret_cast<const uint64_t *>(fw_smem + woff + kHashSlots);
+    const bool k256 = k == 256;
+    const uint64_t cinc = k256 ? 0 : (uint64_t)(128u >> (31 - __clz(k))) * GOLDEN;
+    uint64_t cg = 0;
+    double carry = 0.0;
+    uint32_t cand = 0, cand_u = 0;
+    for (uint32_t t = 0; t < ntiles; t++) {
+        const uint32_t x = t * 128 + lane * 4;  // slot of element 0 of this lane
+        const uint4 u4 = nu;
+        float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
+        if (x < span) {
+            if (a.weighted) w4 = ldg(W4 + (x >> 2));
+            if (x + 128 < span) nu = ldg(T4 + ((x + 128) >> 2));  // next tile's targets
+        }
+        const int32_t i0 = (int32_t)x - (int32_t)off;
+        const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
+        uint32_t valid = 0, isp = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            valid |= ((uint32_t)(i0 + e) < deg ? 1u : 0u) << e;
+            isp |= (u[e] == prev ? 1u : 0u) << e;
+        }
+        const uint32_t need = valid & ~isp;
+        uint32_t mem = 0;
+        if (use_hash) {
+            uint32_t full = 0, pend = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {  // unconditional lookups, masked after
+                const uint4 q = bucket_at(woff, tab_group(u[e], hs));
+                const bool hit = bucket_has(q, u[e]);
+                mem |= (hit ? 1u : 0u) << e;
+                full |= (!hit && q.w < u[e] ? 1u : 0u) << e;
+                pend |= (u[e] > hs.lim ? 1u : 0u) << e;
+            }
+            pend &= need;
+            full &= need & ~pend;
+            if (__any_sync(FULL, full | pend)) {
+                const SlowRet sr =
+                    member4_slow(P, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
+                mem |= sr.mem;
+                hs = sr.hs;
+            }
+        } else {
+            mem = member4_bsearch(P, dp, u[0], u[1], u[2], u[3], need);
+        }
+        // fac[2*is_prev + is_member] = {1/b, 1, 1/a, 1/a}; invalid slots weigh 0
+        const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
+        double wv[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const float w0 = ((valid >> e) & 1) ? (a.weighted ? wf[e] : 1.0f) : 0.0f;
+            const uint32_t fi = (((isp >> e) & 1) << 1) | ((mem >> e) & 1);
+            wv[e] = __dmul_rn(a.fac[fi], (double)w0);
+        }
+        const double p1 = __dadd_rn(wv[0], wv[1]);
+        const double p2 = __dadd_rn(p1, wv[2]);
+        const double p3 = __dadd_rn(p2, wv[3]);
+        const double incl = warp_incl_scan_d(p3, lane);
+        const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
+        carry = __dadd_rn(carry, shfl_d(incl, 31));
+        const uint32_t tau = k256 ? (t & 1) : 0;
+        const uint4 qa = reinterpret_cast<const uint4 *>(Wst)[tau * 64 + lane];
+        const uint4 qb = reinterpret_cast<const uint4 *>(Wst)[tau * 64 + 32 + lane];
+        const uint64_t wd[4] = {(((uint64_t)qa.y << 32) | qa.x) + cg,
+                                (((uint64_t)qa.w << 32) | qa.z) + cg,
+                                (((uint64_t)qb.y << 32) | qb.x) + cg,
+                                (((uint64_t)qb.w << 32) | qb.z) + cg};
+        cg += k256 ? ((t & 1) ? GOLDEN : 0) : cinc;
+        const double pre[4] = {wv[0], p1, p2, p3};
+#if FW_PREFILTER
+        // Accept prefilter.  Element e is accepted iff w > 0 and fl(r*P) < w
+        // with P = base + pre[e] >= base + w, which implies r < w/(base + w)
+        // <= wmax/(base + wmax) = T, i.e. hi32(z) <= floor(T*2^32).  hi32(z)
+        // differs from hi32(y) (y = the second multiply, before the final
+        // xorshift) only in bit 0, so the fast path stops after the second
+        // multiply's high word and compares it against thr >= floor(T*2^32)+2
+        // (base = 0 -> all pass).  Elements that pass run the exact test.
+        const uint32_t thr = accept_thr(a.accept_wmax, base);
+        uint32_t pass = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;
+        pass &= valid;
+        if (pass) {
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                if ((pass >> e) & 1) {
+                    const double r = u01_word(wd[e]);
+                    const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
+                    if (wv[e] > 0.0 && Pr < wv[e]) {
+                        cand = (uint32_t)(i0 + e) + 1;
+                        cand_u = u[e];
+                    }
+                }
+            }
+        }
+#else
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const double r = u01_word(wd[e]);
+            const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
+            if (wv[e] > 0.0 && Pr < wv[e]) {
+                cand = (uint32_t)(i0 + e) + 1;
+                cand_u = u[e];
+            }
+        }
+#endif
+    }
+    const uint32_t sel = __reduce_max_sync(FULL, cand);
+    const unsigned who = __ballot_sync(FULL, cand == sel);
+    sel_u = __shfl_sync(FULL, cand_u, __ffs(who) - 1);
+    __syncwarp();  // the table and the staged words are rebuilt by the next step
+    return sel;
+}
+
+// Node2Vec DPRS, exact order, prev >= 0, any k (lane bases recomputed per
+// element; the correctness path for non-power-of-two lane widths).
 template <int KMODE>
 __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                    uint32_t woff, uint32_t &sel_u) {
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
     const uint32_t off = (uint32_t)(s.elo & 3);
-    if constexpr (KMODE == 2) {
-        const uint32_t nl = min(k, deg), kq = k >> 2;
-        uint64_t *sb = reinterpret_cast<uint64_t *>(fw_smem + woff + kHashSlots);
-        for (uint32_t j = lane; j < nl; j += 32) sb[(j & 3) * kq + (j >> 2)] = lane_base(a, s, j);
-    }
     const uint32_t *P = a.tgt + s.plo;
     const uint32_t dp = (uint32_t)(s.phi - s.plo);
     const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
-    // tile 0's targets are requested before the table build so the two
-    // memory round trips of a step's prologue overlap
     const uint32_t span = deg + off;
     const uint32_t ntiles = (span + 127) >> 7;
     const int64_t ebase = s.elo - off;
     uint4 nu = make_uint4(0, 0, 0, 0);
     if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + lane);
-    uint32_t lim = 0, hshift = 0;
-    if (use_hash) {
-        const HashState hs = hash_build(P, 0, dp, woff, lane);
-        hshift = hs.hshift;
-        lim = hs.lim;
-    } else {
-        __syncwarp();
-    }
+    HashState hs{0, 0, 0};
+    if (use_hash) hs = hash_build(P, 0, dp, woff, lane);
+    else __syncwarp();
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
     for (uint32_t t = 0; t < ntiles; t++) {
@@ -630,27 +826,23 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
             uint32_t here = 0, full = 0;
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                if (((need >> e) & 1) && u[e] <= lim) {
+                if (((need >> e) & 1) && u[e] <= hs.lim) {
                     here |= 1u << e;
-                    const uint4 q = bucket_at(woff, hbucket(u[e], hshift));
+                    const uint4 q = bucket_at(woff, tab_group(u[e], hs));
                     if (bucket_has(q, u[e])) mem |= 1u << e;
-                    else if (q.w != kEmpty) full |= 1u << e;
+                    else if (q.w < u[e]) full |= 1u << e;
                 }
             }
             const uint32_t pend = need & ~here;
             if (__any_sync(FULL, full | pend)) {
-                const SlowRet sr = member4_slow(P, woff, u[0], u[1], u[2], u[3], full, pend,
-                                                hshift, lim, lane);
+                const SlowRet sr =
+                    member4_slow(P, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
                 mem |= sr.mem;
-                hshift = sr.hshift;
-                lim = sr.lim;
+                hs = sr.hs;
             }
         } else {
             mem = member4_bsearch(P, dp, u[0], u[1], u[2], u[3], need);
         }
-        // invalid slots get weight 0 before the conversion (one float select
-        // instead of a double select); the factor comes from the launch's
-        // constant table fac[2*is_prev + is_member] = {1/b, 1, 1/a, 1/a}
         const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
         double wv[4];
 #pragma unroll
@@ -669,16 +861,7 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const uint32_t i = (uint32_t)(i0 + e);
-            uint64_t wd;
-            if constexpr (KMODE == 2) {
-                const uint32_t kq = k >> 2;
-                const uint64_t *sb = reinterpret_cast<const uint64_t *>(fw_smem + woff + kHashSlots);
-                wd = sb[((uint32_t)(e - (int)off) & 3u) * kq + ((i >> 2) & (kq - 1))] +
-                     (uint64_t)(i >> (31 - __clz(k))) * GOLDEN;
-            } else {
-                wd = lane_base(a, s, i % k) + (uint64_t)(i / k) * GOLDEN;
-            }
-            const double r = u01_word(wd);
+            const double r = u01(lane_base(a, s, i % k), (uint64_t)(i / k));
             const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
             if (wv[e] > 0.0 && Pr < wv[e]) {
                 cand = i + 1;
@@ -789,7 +972,7 @@ walk_kernel(const WalkArgs a) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0)
-                            sel = dprs_n2v_exact<2>(a, s, k, lane, woff, sel_u);
+                            sel = dprs_n2v_pow2(a, s, k, lane, woff, sel_u);
                         else
                             sel = dprs_n2v_exact<0>(a, s, k, lane, woff, sel_u);
                         have_u = true;

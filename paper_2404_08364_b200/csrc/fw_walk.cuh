@@ -36,8 +36,8 @@ struct WalkArgs {
     double fac[4];  // node2vec factor by 2*is_prev + is_member: {1/b, 1, 1/a, 1/a}
     int64_t k_small, k_big, d_t;
     uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
-    uint32_t merge_ratio;
-    uint32_t n2v_mode;  // 0: two-pass early-exit DPRS (default), 1: single forward pass  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
+    uint32_t merge_ratio;  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
+    float accept_wmax;     // upper bound on any app weight (exact node2vec accept prefilter)
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };

@@ -27,7 +27,7 @@ namespace fw {
 // Inlined by default: an out-of-line call makes the tile loop save and
 // restore registers around it (measured 6.3e7 vs 5.4e7 steps/s).
 #ifndef FW_PREFILTER
-#define FW_PREFILTER 0
+#define FW_PREFILTER 1
 #endif
 
 #ifdef FW_COLD_OUTLINE
@@ -422,6 +422,27 @@ __device__ __forceinline__ double scan_round(double v, int lane) {
         : "+d"(v) : "r"(lane), "n"(D), "d"(o));
     return v;
 }
+// Same scan, with the add predicated on the shuffle's own in-range flag (no
+// lane-index register needed).
+template <int D>
+__device__ __forceinline__ double scan_round_p(double v) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t.reg .f64 o;\n\t"
+        "mov.b64 {lo, hi}, %0;\n\t"
+        "shfl.sync.up.b32 lo|p, lo, %1, 0, -1;\n\t"
+        "shfl.sync.up.b32 hi, hi, %1, 0, -1;\n\t"
+        "mov.b64 o, {lo, hi};\n\t"
+        "@p add.rn.f64 %0, %0, o;\n\t}"
+        : "+d"(v) : "n"(D));
+    return v;
+}
+__device__ __forceinline__ double warp_incl_scan_p(double v) {
+    v = scan_round_p<1>(v);
+    v = scan_round_p<2>(v);
+    v = scan_round_p<4>(v);
+    v = scan_round_p<8>(v);
+    return scan_round_p<16>(v);
+}
+
 __device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
     v = scan_round<1>(v, lane);
     v = scan_round<2>(v, lane);
@@ -516,7 +537,11 @@ struct SlowRet {
     HashState hs;
 };
 
-__device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ P, uint32_t woff,
+__device__ __forceinline__ int64_t ctl_plo(uint32_t woff) {
+    return (int64_t)(((uint64_t)fw_smem[woff + kCtlWord + 5] << 32) | fw_smem[woff + kCtlWord + 4]);
+}
+
+__device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ tgt, uint32_t woff,
                                         uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3,
                                         uint32_t full, uint32_t need, HashState hs, int lane) {
     const uint32_t u[4] = {u0, u1, u2, u3};
@@ -540,6 +565,7 @@ __device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ P, uint32_t
             if ((need >> e) & 1) umin = u[e];
         umin = __reduce_min_sync(FULL, umin);
         // advance: skip whole chunks that end below every pending u
+        const uint32_t *P = tgt + ctl_plo(woff);
         const uint32_t dp = fw_smem[woff + kCtlWord + 2];
         uint32_t c0 = fw_smem[woff + kCtlWord + 0] + fw_smem[woff + kCtlWord + 1];
         while (c0 + kChunk < dp && ldg(P + c0 + kChunk - 1) < umin) c0 += kChunk;
@@ -652,34 +678,35 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
     const uint32_t off = (uint32_t)(s.elo & 3);
-    const uint32_t *P = a.tgt + s.plo;
     const uint32_t dp = (uint32_t)(s.phi - s.plo);
     const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
     const uint32_t span = deg + off;
-    const uint32_t ntiles = (span + 127) >> 7;
     const int64_t ebase = s.elo - off;
-    const uint4 *T4 = reinterpret_cast<const uint4 *>(a.tgt + ebase);
-    const float4 *W4 = reinterpret_cast<const float4 *>(a.w + ebase);
+    // N(prev)'s start lives in the control words (read by the cold paths)
+    if (lane == 0) {
+        fw_smem[woff + kCtlWord + 4] = (uint32_t)s.plo;
+        fw_smem[woff + kCtlWord + 5] = (uint32_t)((uint64_t)s.plo >> 32);
+    }
     // tile 0's targets are requested before the table build so the memory
     // round trips of a step's prologue overlap
     uint4 nu = make_uint4(0, 0, 0, 0);
-    if ((uint32_t)lane * 4 < span) nu = ldg(T4 + lane);
+    if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + lane);
     stage_words(a, s, k, lane, woff, off);
     HashState hs{0, 0, 0};
-    if (use_hash) hs = hash_build(P, 0, dp, woff, lane);
-    const uint64_t *Wst = reinterpret_cast<const uint64_t *>(fw_smem + woff + kHashSlots);
-    const bool k256 = k == 256;
-    const uint64_t cinc = k256 ? 0 : (uint64_t)(128u >> (31 - __clz(k))) * GOLDEN;
-    uint64_t cg = 0;
+    if (use_hash) hs = hash_build(a.tgt + s.plo, 0, dp, woff, lane);
+    // counter of tile t: k == 256 -> t >> 1; k <= 128 -> t * (128 / k)
+    const uint32_t cmul = k == 256 ? 0 : (128u >> (31 - __clz(k)));
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
-    for (uint32_t t = 0; t < ntiles; t++) {
-        const uint32_t x = t * 128 + lane * 4;  // slot of element 0 of this lane
+    for (uint32_t x = (uint32_t)lane * 4; x - (uint32_t)lane * 4 < span; x += 128) {
+        // x = slot of this lane's element 0 in tile t = x >> 7
+        const uint32_t t = x >> 7;
         const uint4 u4 = nu;
         float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
         if (x < span) {
-            if (a.weighted) w4 = ldg(W4 + (x >> 2));
-            if (x + 128 < span) nu = ldg(T4 + ((x + 128) >> 2));  // next tile's targets
+            if (a.weighted) w4 = ldg(reinterpret_cast<const float4 *>(a.w + ebase) + (x >> 2));
+            if (x + 128 < span)  // next tile's targets
+                nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + ((x + 128) >> 2));
         }
         const int32_t i0 = (int32_t)x - (int32_t)off;
         const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
@@ -705,12 +732,12 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             full &= need & ~pend;
             if (__any_sync(FULL, full | pend)) {
                 const SlowRet sr =
-                    member4_slow(P, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
+                    member4_slow(a.tgt, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
                 mem |= sr.mem;
                 hs = sr.hs;
             }
         } else {
-            mem = member4_bsearch(P, dp, u[0], u[1], u[2], u[3], need);
+            mem = member4_bsearch(a.tgt + ctl_plo(woff), dp, u[0], u[1], u[2], u[3], need);
         }
         // fac[2*is_prev + is_member] = {1/b, 1, 1/a, 1/a}; invalid slots weigh 0
         const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
@@ -724,17 +751,19 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         const double p1 = __dadd_rn(wv[0], wv[1]);
         const double p2 = __dadd_rn(p1, wv[2]);
         const double p3 = __dadd_rn(p2, wv[3]);
-        const double incl = warp_incl_scan_d(p3, lane);
+        const double incl = warp_incl_scan_p(p3);
         const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
         carry = __dadd_rn(carry, shfl_d(incl, 31));
-        const uint32_t tau = k256 ? (t & 1) : 0;
-        const uint4 qa = reinterpret_cast<const uint4 *>(Wst)[tau * 64 + lane];
-        const uint4 qb = reinterpret_cast<const uint4 *>(Wst)[tau * 64 + 32 + lane];
+        // draw words: staged per-lane words + counter(t) * GOLDEN
+        const uint32_t tau = cmul ? 0 : (t & 1);
+        const uint4 *wq = reinterpret_cast<const uint4 *>(fw_smem + woff + kHashSlots) +
+                          tau * 64 + (x & 127) / 4;
+        const uint4 qa = wq[0], qb = wq[32];
+        const uint64_t cg = (uint64_t)(cmul ? t * cmul : t >> 1) * GOLDEN;
         const uint64_t wd[4] = {(((uint64_t)qa.y << 32) | qa.x) + cg,
                                 (((uint64_t)qa.w << 32) | qa.z) + cg,
                                 (((uint64_t)qb.y << 32) | qb.x) + cg,
                                 (((uint64_t)qb.w << 32) | qb.z) + cg};
-        cg += k256 ? ((t & 1) ? GOLDEN : 0) : cinc;
         const double pre[4] = {wv[0], p1, p2, p3};
 #if FW_PREFILTER
         // Accept prefilter.  Element e is accepted iff w > 0 and fl(r*P) < w
@@ -748,8 +777,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         uint32_t pass = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;
-        pass &= valid;
-        if (pass) {
+        if (pass & valid) {
 #pragma unroll
             for (int e = 0; e < 4; e++) {
                 if ((pass >> e) & 1) {
@@ -797,6 +825,10 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
     const int64_t ebase = s.elo - off;
     uint4 nu = make_uint4(0, 0, 0, 0);
     if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + lane);
+    if (lane == 0) {
+        fw_smem[woff + kCtlWord + 4] = (uint32_t)s.plo;
+        fw_smem[woff + kCtlWord + 5] = (uint32_t)((uint64_t)s.plo >> 32);
+    }
     HashState hs{0, 0, 0};
     if (use_hash) hs = hash_build(P, 0, dp, woff, lane);
     else __syncwarp();
@@ -836,7 +868,7 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
             const uint32_t pend = need & ~here;
             if (__any_sync(FULL, full | pend)) {
                 const SlowRet sr =
-                    member4_slow(P, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
+                    member4_slow(a.tgt, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
                 mem |= sr.mem;
                 hs = sr.hs;
             }
@@ -912,7 +944,7 @@ __device__ __forceinline__ void stat_add(unsigned long long *st, int idx, long l
 // The persistent walker.
 // ---------------------------------------------------------------------------
 template <int APP, int SAMPLER, bool EXACT>
-__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks)
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks(APP))
 walk_kernel(const WalkArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t woff = (threadIdx.x >> 5) * kWarpSmemWords;

@@ -4,17 +4,26 @@
 
 namespace fw {
 
-constexpr int kWalkThreads = 256;  // 8 warp walkers per CTA
-#ifndef FW_MIN_BLOCKS
-#define FW_MIN_BLOCKS 4
+#ifndef FW_WALK_THREADS
+#define FW_WALK_THREADS 128
 #endif
-constexpr int kWalkMinBlocks = FW_MIN_BLOCKS;  // >= 32 resident warps per SM
+constexpr int kWalkThreads = FW_WALK_THREADS;  // 4 warp walkers per CTA
+// Resident CTAs per SM the register budget is sized for.  Node2Vec's tile
+// loop runs at 72 registers / 28 warps per SM (measured faster than 64 / 32
+// and 80 / 24); the first-order apps at 64 / 32.
+#ifndef FW_MIN_BLOCKS
+#define FW_MIN_BLOCKS 8
+#endif
+#ifndef FW_MIN_BLOCKS_N2V
+#define FW_MIN_BLOCKS_N2V 7
+#endif
+constexpr int walk_min_blocks(int app) { return app == 2 ? FW_MIN_BLOCKS_N2V : FW_MIN_BLOCKS; }
 // per-warp shared memory: N(prev) hash window + 256 staged lane bases
 constexpr uint32_t kHashSlots = 1024;
 constexpr uint32_t kChunk = 256;  // N(prev) entries hashed at a time (load <= 1/4)
 constexpr uint32_t kStatsWord = kHashSlots + 2 * 256;    // 8 x u64 RunStats counters
 constexpr uint32_t kCtlWord = kStatsWord + 2 * 8;       // hash window control words
-constexpr uint32_t kWarpSmemWords = kCtlWord + 4;
+constexpr uint32_t kWarpSmemWords = kCtlWord + 8;  // [4],[5]: N(prev) start (node2vec)
 constexpr int kWalkSmemBytes = (kWalkThreads / 32) * kWarpSmemWords * 4;
 
 // Kernel arguments (passed by value through the constant bank).

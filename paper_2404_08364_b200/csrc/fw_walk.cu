@@ -36,7 +36,7 @@ namespace fw {
 #define FW_COLD __forceinline__
 #endif
 
-// Dynamic shared memory: kWarpSmemWords words per warp (see fw_walk.cuh).
+// Dynamic shared memory: warp_words(APP) words per warp (see fw_walk.cuh).
 extern __shared__ __align__(16) uint32_t fw_smem[];
 
 struct StepCtx {
@@ -460,14 +460,14 @@ __device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
 // and key i goes to slot pos_i = i + max_{j<=i}(4 b_j - j): the first free
 // slot at or after its group start, keeping the table sorted (a warp
 // max-scan, no atomics, no collisions).  pos_i <= 4(kGroups-1) + cn - 1 <
-// kHashSlots.  A lookup reads group b(u) with one LDS.128; u is present iff
+// kTabSlots.  A lookup reads group b(u) with one LDS.128; u is present iff
 // it is in that group, or -- when the group is full and its last key is < u
 // (rare) -- in a following group.  Empty slots hold kEmpty (> any vertex
 // id).  The window over N(prev) is described by three registers in the hot
 // loop (kmin, scale, lim = kmax or ~0 for the last chunk); chunk start,
 // length and d(prev) sit in the warp's control words (kCtlWord).
-constexpr uint32_t kGroups = 192;
-static_assert(4 * (kGroups - 1) + kChunk <= kHashSlots, "table overflow");
+constexpr uint32_t kGroups = 304;
+static_assert(4 * (kGroups - 1) + kChunk <= kTabSlots, "table overflow");
 
 struct HashState {
     uint32_t kmin, scale, lim;
@@ -501,8 +501,9 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t
     __syncwarp();  // previous readers of the table are done
     uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + woff);
 #pragma unroll
-    for (int x = 0; x < (int)(kHashSlots / 128); x++)
-        t4[x * 32 + lane] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    for (int x = 0; x < (int)((kTabSlots / 4 + 31) / 32); x++)
+        if (x * 32 + lane < (int)(kTabSlots / 4))
+            t4[x * 32 + lane] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     if (lane == 0) {
         fw_smem[woff + kCtlWord + 0] = c0;
         fw_smem[woff + kCtlWord + 1] = cn;
@@ -511,7 +512,7 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t
     HashState hs;
     hs.kmin = __shfl_sync(FULL, keys[0], 0);
     const float range = (float)(kmax - hs.kmin) + 1.0f;
-    hs.scale = (uint32_t)fminf((float)kGroups * 4294967296.0f / range, 4294967040.0f);
+    hs.scale = (uint32_t)fminf(__fdividef((float)kGroups * 4294967296.0f, range), 4294967040.0f);
     hs.lim = c0 + cn >= dp ? kEmpty : kmax;
     __syncwarp();
     int carry = INT_MIN;
@@ -642,7 +643,7 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t x, int src) {
 // conflict-free LDS.128 per tile.
 __device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s, uint32_t k,
                                             int lane, uint32_t woff, uint32_t off) {
-    uint64_t *W = reinterpret_cast<uint64_t *>(fw_smem + woff + kHashSlots);
+    uint64_t *W = reinterpret_cast<uint64_t *>(fw_smem + woff + kTabSlots);
     const uint32_t lk = 31 - __clz(k);
     if (k <= 32) {
         const uint64_t b = (uint32_t)lane < k ? lane_base(a, s, lane) : 0;
@@ -756,7 +757,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         carry = __dadd_rn(carry, shfl_d(incl, 31));
         // draw words: staged per-lane words + counter(t) * GOLDEN
         const uint32_t tau = cmul ? 0 : (t & 1);
-        const uint4 *wq = reinterpret_cast<const uint4 *>(fw_smem + woff + kHashSlots) +
+        const uint4 *wq = reinterpret_cast<const uint4 *>(fw_smem + woff + kTabSlots) +
                           tau * 64 + (x & 127) / 4;
         const uint4 qa = wq[0], qb = wq[32];
         const uint64_t cg = (uint64_t)(cmul ? t * cmul : t >> 1) * GOLDEN;
@@ -947,11 +948,11 @@ template <int APP, int SAMPLER, bool EXACT>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks(APP))
 walk_kernel(const WalkArgs a) {
     const int lane = threadIdx.x & 31;
-    const uint32_t woff = (threadIdx.x >> 5) * kWarpSmemWords;
+    const uint32_t woff = (threadIdx.x >> 5) * warp_words(APP);
     // per-warp RunStats counters live in shared memory (registers are the
     // scarce resource in the sampler loops); every lane keeps the same value
     // in flight, lane 0 owns the slot.
-    unsigned long long *st = reinterpret_cast<unsigned long long *>(fw_smem + woff + kStatsWord);
+    unsigned long long *st = reinterpret_cast<unsigned long long *>(fw_smem + woff + stats_word(APP));
     if (lane < ST_COUNT) st[lane] = 0;
     __syncwarp();
 
@@ -1067,10 +1068,10 @@ static cudaError_t launch_t(const WalkArgs &a, int grid, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, EXACT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmemBytes);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, walk_smem_bytes(APP));
         attr = true;
     }
-    walk_kernel<APP, SAMPLER, EXACT><<<grid, kWalkThreads, kWalkSmemBytes, stream>>>(a);
+    walk_kernel<APP, SAMPLER, EXACT><<<grid, kWalkThreads, walk_smem_bytes(APP), stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -1078,9 +1079,9 @@ template <int APP, int SAMPLER, bool EXACT>
 static int occupancy_t() {
     int nb = 0;
     cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, EXACT>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmemBytes);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, walk_smem_bytes(APP));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_kernel<APP, SAMPLER, EXACT>,
-                                                  kWalkThreads, kWalkSmemBytes);
+                                                  kWalkThreads, walk_smem_bytes(APP));
     return nb;
 }
 

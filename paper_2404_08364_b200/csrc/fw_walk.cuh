@@ -18,13 +18,22 @@ constexpr int kWalkThreads = FW_WALK_THREADS;  // 4 warp walkers per CTA
 #define FW_MIN_BLOCKS_N2V 7
 #endif
 constexpr int walk_min_blocks(int app) { return app == 2 ? FW_MIN_BLOCKS_N2V : FW_MIN_BLOCKS; }
-// per-warp shared memory: N(prev) hash window + 256 staged lane bases
+// Per-warp shared memory (32-bit words):
+//   [0, slots)            first-order apps: ZPRS weight staging (kHashSlots);
+//                         node2vec: the N(prev) window table (kTabSlots)
+//   [slots, +512)         256 x u64: ZPRS lane prefixes / node2vec draw words
+//   [stats, +16)          8 x u64 RunStats counters
+//   [ctl, +8)             node2vec window control words; [4],[5]: N(prev) start
+// node2vec's larger table keeps 28 warps (7 CTAs x 4) resident per SM.
 constexpr uint32_t kHashSlots = 1024;
-constexpr uint32_t kChunk = 256;  // N(prev) entries hashed at a time (load <= 1/4)
-constexpr uint32_t kStatsWord = kHashSlots + 2 * 256;    // 8 x u64 RunStats counters
-constexpr uint32_t kCtlWord = kStatsWord + 2 * 8;       // hash window control words
-constexpr uint32_t kWarpSmemWords = kCtlWord + 8;  // [4],[5]: N(prev) start (node2vec)
-constexpr int kWalkSmemBytes = (kWalkThreads / 32) * kWarpSmemWords * 4;
+constexpr uint32_t kTabSlots = 1472;
+constexpr uint32_t kChunk = 256;  // N(prev) entries per table window
+__host__ __device__ constexpr uint32_t warp_slots(int app) { return app == 2 ? kTabSlots : kHashSlots; }
+__host__ __device__ constexpr uint32_t stats_word(int app) { return warp_slots(app) + 2 * 256; }
+__host__ __device__ constexpr uint32_t ctl_word(int app) { return stats_word(app) + 2 * 8; }
+__host__ __device__ constexpr uint32_t warp_words(int app) { return ctl_word(app) + 8; }
+__host__ __device__ constexpr int walk_smem_bytes(int app) { return (kWalkThreads / 32) * warp_words(app) * 4; }
+constexpr uint32_t kCtlWord = ctl_word(2);  // node2vec control words
 
 // Kernel arguments (passed by value through the constant bank).
 struct WalkArgs {

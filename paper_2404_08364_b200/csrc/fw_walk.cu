@@ -682,7 +682,10 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     const uint32_t dp = (uint32_t)(s.phi - s.plo);
     const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
     const uint32_t span = deg + off;
-    const int64_t ebase = s.elo - off;
+    // this lane's 4-slot group of tile 0 (16-byte aligned: the tile grid is
+    // anchored at elo & ~3); weights sit at a fixed byte distance
+    const uint32_t *tp = a.tgt + (s.elo - off) + 4 * lane;
+    const int64_t wdelta = reinterpret_cast<const char *>(a.w) - reinterpret_cast<const char *>(a.tgt);
     // N(prev)'s start lives in the control words (read by the cold paths)
     if (lane == 0) {
         fw_smem[woff + kCtlWord + 4] = (uint32_t)s.plo;
@@ -691,46 +694,51 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     // tile 0's targets are requested before the table build so the memory
     // round trips of a step's prologue overlap
     uint4 nu = make_uint4(0, 0, 0, 0);
-    if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + lane);
+    if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(tp));
     stage_words(a, s, k, lane, woff, off);
     HashState hs{0, 0, 0};
     if (use_hash) hs = hash_build(a.tgt + s.plo, 0, dp, woff, lane);
     // counter of tile t: k == 256 -> t >> 1; k <= 128 -> t * (128 / k)
     const uint32_t cmul = k == 256 ? 0 : (128u >> (31 - __clz(k)));
+    const uint32_t wq0 = (woff + kTabSlots) * 4 + 16 * lane;  // staged words (bytes)
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;
-    for (uint32_t x = (uint32_t)lane * 4; x - (uint32_t)lane * 4 < span; x += 128) {
-        // x = slot of this lane's element 0 in tile t = x >> 7
-        const uint32_t t = x >> 7;
+    const uint32_t ntiles = (span + 127) >> 7;
+    for (uint32_t t = 0; t < ntiles; t++, tp += 128) {
+        const uint32_t x0 = t * 128;  // first slot of the tile
+        // interior tile: all 128 slots are elements of N(cur)
+        const bool edge = x0 < off || x0 + 128 > span;
         const uint4 u4 = nu;
-        float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (x < span) {
-            if (a.weighted) w4 = ldg(reinterpret_cast<const float4 *>(a.w + ebase) + (x >> 2));
-            if (x + 128 < span)  // next tile's targets
-                nu = ldg(reinterpret_cast<const uint4 *>(a.tgt + ebase) + ((x + 128) >> 2));
-        }
-        const int32_t i0 = (int32_t)x - (int32_t)off;
         const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
-        uint32_t valid = 0, isp = 0;
+        const int32_t i0 = (int32_t)(x0 + 4 * lane) - (int32_t)off;
+        float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
+        uint32_t valid = 0xF;
+        if (edge) {
+            if (x0 + 4 * lane < span && a.weighted)
+                w4 = ldg(reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(tp) + wdelta));
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-            valid |= ((uint32_t)(i0 + e) < deg ? 1u : 0u) << e;
-            isp |= (u[e] == prev ? 1u : 0u) << e;
+            for (int e = 0; e < 4; e++) valid &= ~(((uint32_t)(i0 + e) < deg ? 0u : 1u) << e);
+        } else if (a.weighted) {
+            w4 = ldg(reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(tp) + wdelta));
         }
-        const uint32_t need = valid & ~isp;
+        if (x0 + 128 < span && x0 + 128 + 4 * lane < span)  // next tile's targets
+            nu = ldg(reinterpret_cast<const uint4 *>(tp + 128));
         uint32_t mem = 0;
         if (use_hash) {
+            // lookups for every slot (prev's and invalid slots' results are
+            // ignored below); trouble = some valid slot beyond the window or
+            // in a full group whose last key is < u
             uint32_t full = 0, pend = 0;
 #pragma unroll
-            for (int e = 0; e < 4; e++) {  // unconditional lookups, masked after
+            for (int e = 0; e < 4; e++) {
                 const uint4 q = bucket_at(woff, tab_group(u[e], hs));
                 const bool hit = bucket_has(q, u[e]);
                 mem |= (hit ? 1u : 0u) << e;
                 full |= (!hit && q.w < u[e] ? 1u : 0u) << e;
                 pend |= (u[e] > hs.lim ? 1u : 0u) << e;
             }
-            pend &= need;
-            full &= need & ~pend;
+            pend &= valid;
+            full &= valid & ~pend;
             if (__any_sync(FULL, full | pend)) {
                 const SlowRet sr =
                     member4_slow(a.tgt, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
@@ -738,16 +746,16 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                 hs = sr.hs;
             }
         } else {
-            mem = member4_bsearch(a.tgt + ctl_plo(woff), dp, u[0], u[1], u[2], u[3], need);
+            mem = member4_bsearch(a.tgt + ctl_plo(woff), dp, u[0], u[1], u[2], u[3], valid);
         }
         // fac[2*is_prev + is_member] = {1/b, 1, 1/a, 1/a}; invalid slots weigh 0
         const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
         double wv[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            const float w0 = ((valid >> e) & 1) ? (a.weighted ? wf[e] : 1.0f) : 0.0f;
-            const uint32_t fi = (((isp >> e) & 1) << 1) | ((mem >> e) & 1);
-            wv[e] = __dmul_rn(a.fac[fi], (double)w0);
+            const float w0 = ((valid >> e) & 1) ? wf[e] : 0.0f;
+            const double f = u[e] == prev ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
+            wv[e] = __dmul_rn(f, (double)w0);
         }
         const double p1 = __dadd_rn(wv[0], wv[1]);
         const double p2 = __dadd_rn(p1, wv[2]);
@@ -756,10 +764,9 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
         carry = __dadd_rn(carry, shfl_d(incl, 31));
         // draw words: staged per-lane words + counter(t) * GOLDEN
-        const uint32_t tau = cmul ? 0 : (t & 1);
-        const uint4 *wq = reinterpret_cast<const uint4 *>(fw_smem + woff + kTabSlots) +
-                          tau * 64 + (x & 127) / 4;
-        const uint4 qa = wq[0], qb = wq[32];
+        const uint32_t wq = wq0 + (cmul ? 0 : (t & 1) * 1024);
+        const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
+        const uint4 qb = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq + 512);
         const uint64_t cg = (uint64_t)(cmul ? t * cmul : t >> 1) * GOLDEN;
         const uint64_t wd[4] = {(((uint64_t)qa.y << 32) | qa.x) + cg,
                                 (((uint64_t)qa.w << 32) | qa.z) + cg,

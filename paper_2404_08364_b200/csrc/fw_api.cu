@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cfloat>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -383,6 +384,28 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         float f = (float)wm;
         if ((double)f < wm) f = std::nextafter(f, INFINITY);
         a.accept_wmax = (std::isfinite(f) && f <= 1e37f) ? f : INFINITY;  // inf: prefilter off
+    }
+    {   // fp32 factor path: 1/a, 1/b = 2^k and every w * 2^k exact in fp32
+        auto pow2_exp = [](double f, int *k) {
+            int e;
+            const double m = std::frexp(f, &e);
+            *k = e - 1;
+            return f > 0.0 && m == 0.5;
+        };
+        int ka = 0, kb = 0;
+        bool ok = app->app_id == FW_APP_NODE2VEC && pow2_exp(app->inv_a, &ka) &&
+                  pow2_exp(app->inv_b, &kb) && std::abs(ka) <= 16 && std::abs(kb) <= 16;
+        if (ok && app->weighted) {
+            const int kmin = std::min({0, ka, kb}), kmax = std::max({0, ka, kb});
+            ok = !g->info.reserved &&
+                 (!(g->info.max_weight > 0.0f) ||
+                  ((long)g->info.min_weight_lowbit_exp + kmin >= -149 &&
+                   std::ldexp((double)g->info.max_weight, kmax) <= (double)FLT_MAX));
+        }
+        const char *env = getenv("FW_FAC32");  // A/B override: 0 forces the fp64 factor path
+        a.fac32 = ok && !(env && env[0] == '0') ? 1 : 0;
+        a.inv_a32 = (float)app->inv_a;
+        a.inv_b32 = (float)app->inv_b;
     }
     a.k_small = eng->k_small;
     a.k_big = eng->k_big;

@@ -674,6 +674,7 @@ __device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s,
 // ahead) and weights, branch-free membership lookups into the N(prev) table,
 // a 4-element local prefix plus one warp scan, draw words from the staged
 // per-lane table, and the accept test.
+template <bool F32>
 __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                   uint32_t woff, uint32_t &sel_u) {
     const uint32_t deg = s.deg;
@@ -711,29 +712,46 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         const uint4 u4 = nu;
         const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
         const int32_t i0 = (int32_t)(x0 + 4 * lane) - (int32_t)off;
-        float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
+        float wf[4] = {1.f, 1.f, 1.f, 1.f};
         uint32_t valid = 0xF;
         if (edge) {
-            if (x0 + 4 * lane < span && a.weighted)
-                w4 = ldg(reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(tp) + wdelta));
+            if (x0 + 4 * lane < span && a.weighted) {
+                const float4 w4 = ldg(reinterpret_cast<const float4 *>(
+                    reinterpret_cast<const char *>(tp) + wdelta));
+                wf[0] = w4.x; wf[1] = w4.y; wf[2] = w4.z; wf[3] = w4.w;
+            }
 #pragma unroll
-            for (int e = 0; e < 4; e++) valid &= ~(((uint32_t)(i0 + e) < deg ? 0u : 1u) << e);
+            for (int e = 0; e < 4; e++) {  // invalid slots weigh 0
+                if ((uint32_t)(i0 + e) >= deg) {
+                    valid &= ~(1u << e);
+                    wf[e] = 0.0f;
+                }
+            }
         } else if (a.weighted) {
-            w4 = ldg(reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(tp) + wdelta));
+            const float4 w4 = ldg(reinterpret_cast<const float4 *>(
+                reinterpret_cast<const char *>(tp) + wdelta));
+            wf[0] = w4.x; wf[1] = w4.y; wf[2] = w4.z; wf[3] = w4.w;
         }
         if (x0 + 128 < span && x0 + 128 + 4 * lane < span)  // next tile's targets
             nu = ldg(reinterpret_cast<const uint4 *>(tp + 128));
+        // membership u in N(prev) and the app weight (_kernels.py:288-306):
+        // factor 1/a if u == prev, else 1 if u in N(prev), else 1/b
         uint32_t mem = 0;
+        float wp[4];  // F32: factor * w, exact in fp32
         if (use_hash) {
             // lookups for every slot (prev's and invalid slots' results are
-            // ignored below); trouble = some valid slot beyond the window or
-            // in a full group whose last key is < u
+            // ignored); the cold path handles valid slots beyond the window
+            // and those in a full group whose last key is < u
             uint32_t full = 0, pend = 0;
 #pragma unroll
             for (int e = 0; e < 4; e++) {
                 const uint4 q = bucket_at(woff, tab_group(u[e], hs));
                 const bool hit = bucket_has(q, u[e]);
-                mem |= (hit ? 1u : 0u) << e;
+                if constexpr (F32) {
+                    wp[e] = (u[e] == prev ? a.inv_a32 : (hit ? 1.0f : a.inv_b32)) * wf[e];
+                } else {
+                    mem |= (hit ? 1u : 0u) << e;
+                }
                 full |= (!hit && q.w < u[e] ? 1u : 0u) << e;
                 pend |= (u[e] > hs.lim ? 1u : 0u) << e;
             }
@@ -742,20 +760,32 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             if (__any_sync(FULL, full | pend)) {
                 const SlowRet sr =
                     member4_slow(a.tgt, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
-                mem |= sr.mem;
                 hs = sr.hs;
+                if constexpr (F32) {
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        if (((sr.mem >> e) & 1) && u[e] != prev) wp[e] = wf[e];
+                } else {
+                    mem |= sr.mem;
+                }
             }
         } else {
             mem = member4_bsearch(a.tgt + ctl_plo(woff), dp, u[0], u[1], u[2], u[3], valid);
+            if constexpr (F32) {
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                    wp[e] = (u[e] == prev ? a.inv_a32 : (((mem >> e) & 1) ? 1.0f : a.inv_b32)) * wf[e];
+            }
         }
-        // fac[2*is_prev + is_member] = {1/b, 1, 1/a, 1/a}; invalid slots weigh 0
-        const float wf[4] = {w4.x, w4.y, w4.z, w4.w};
         double wv[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            const float w0 = ((valid >> e) & 1) ? wf[e] : 0.0f;
-            const double f = u[e] == prev ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
-            wv[e] = __dmul_rn(f, (double)w0);
+            if constexpr (F32) {
+                wv[e] = (double)wp[e];
+            } else {
+                const double f = u[e] == prev ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
+                wv[e] = __dmul_rn(f, (double)wf[e]);
+            }
         }
         const double p1 = __dadd_rn(wv[0], wv[1]);
         const double p2 = __dadd_rn(p1, wv[2]);
@@ -1012,7 +1042,8 @@ walk_kernel(const WalkArgs a) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0)
-                            sel = dprs_n2v_pow2(a, s, k, lane, woff, sel_u);
+                            sel = a.fac32 ? dprs_n2v_pow2<true>(a, s, k, lane, woff, sel_u)
+                                          : dprs_n2v_pow2<false>(a, s, k, lane, woff, sel_u);
                         else
                             sel = dprs_n2v_exact<0>(a, s, k, lane, woff, sel_u);
                         have_u = true;

@@ -56,6 +56,10 @@ struct WalkArgs {
     uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
     uint32_t merge_ratio;  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
     float accept_wmax;     // upper bound on any app weight (exact node2vec accept prefilter)
+    // node2vec: 1/a and 1/b are powers of two and w * {1/a, 1/b} is exact in
+    // fp32 for every weight, so factor * weight is formed in fp32 and widened
+    int32_t fac32;
+    float inv_a32, inv_b32;
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };

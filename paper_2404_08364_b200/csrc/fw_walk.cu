@@ -422,18 +422,20 @@ __device__ __forceinline__ double scan_round(double v, int lane) {
         : "+d"(v) : "r"(lane), "n"(D), "d"(o));
     return v;
 }
-// Same scan, with the add predicated on the shuffle's own in-range flag (no
-// lane-index register needed).
+// Same scan without a lane-index register: the shuffled addend is zeroed
+// (two SELs on its halves) when the shuffle's own in-range flag is clear, so
+// the add is unconditional and both operands stay in aligned register pairs.
 template <int D>
 __device__ __forceinline__ double scan_round_p(double v) {
-    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t.reg .f64 o;\n\t"
-        "mov.b64 {lo, hi}, %0;\n\t"
-        "shfl.sync.up.b32 lo|p, lo, %1, 0, -1;\n\t"
-        "shfl.sync.up.b32 hi, hi, %1, 0, -1;\n\t"
-        "mov.b64 o, {lo, hi};\n\t"
-        "@p add.rn.f64 %0, %0, o;\n\t}"
-        : "+d"(v) : "n"(D));
-    return v;
+    uint32_t olo, ohi;
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "shfl.sync.up.b32 %0|p, %2, %4, 0, -1;\n\t"
+                 "shfl.sync.up.b32 %1, %3, %4, 0, -1;\n\t"
+                 "@!p mov.b32 %0, 0;\n\t"
+                 "@!p mov.b32 %1, 0;\n\t}"
+                 : "=r"(olo), "=r"(ohi)
+                 : "r"(__double2loint(v)), "r"(__double2hiint(v)), "n"(D));
+    return __dadd_rn(v, __hiloint2double(ohi, olo));
 }
 __device__ __forceinline__ double warp_incl_scan_p(double v) {
     v = scan_round_p<1>(v);
@@ -616,12 +618,14 @@ __device__ __forceinline__ uint32_t mix64_yhi(uint64_t z) {
 
 // Prefilter threshold for a lane whose elements all have prefix P >= base + w:
 // >= floor(T * 2^32) + 2 with T = wmax / (base + wmax), saturated.  The fp32
-// estimate of T (conversion, add, approximate divide) is within 2^-20
-// relative; the 2^-12 margin covers it.  base beyond the fp32 range gives
+// estimate of T (conversion, add, approximate reciprocal, multiply) is within
+// 2^-20 relative; the 2^-12 margin covers it.  base beyond the fp32 range gives
 // t = 0 and thr = 2, still >= floor(T * 2^32) + 2 = 2.
 __device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
     const float b = (float)base;
-    const float t = __fdividef(wmax, b + wmax);
+    float r;  // MUFU.RCP without the denormal-range fixup of __fdividef
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b + wmax));
+    const float t = wmax * r;
     const uint32_t thr = __float2uint_rz(fmaf(t, 4294967296.0f * 1.000244140625f, 2.0f));
     return wmax <= 1e37f ? thr : 0xFFFFFFFFu;  // the host passes +inf to disable
 }

@@ -485,21 +485,23 @@ __device__ __forceinline__ bool bucket_has(const uint4 q, uint32_t u) {
     return q.x == u || q.y == u || q.z == u || q.w == u;
 }
 
-// Build the table from P[c0, c0 + min(kChunk, dp - c0)).  Control words:
-// [0] = c0, [1] = cn, [2] = dp.
-__device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t c0,
-                                        uint32_t dp, uint32_t woff, int lane) {
-    const uint32_t cn = min(kChunk, dp - c0);
-    const uint32_t *src = P + c0;
-    // all of this lane's keys are requested first (independent loads)
-    constexpr int kKeys = kChunk / 32;
-    uint32_t keys[kKeys];
-#pragma unroll
-    for (int r = 0; r < kKeys; r++) {
-        const uint32_t x = r * 32 + lane;
-        keys[r] = x < cn ? ldg(src + x) : kEmpty;
-    }
-    const uint32_t kmax = ldg(src + cn - 1);
+// Build the table for chunk c of N(prev) = tgt[plo, plo + dp).  Chunks sit
+// on a 16-byte aligned grid: chunk c covers global slots [A + 256c, A +
+// 256(c+1)) with A = plo & ~3, clipped to N(prev), so lane x reads its 8
+// consecutive slots with two 16-byte loads, forms the running max of
+// 4 b(k_s) - s over them, and one warp max-scan gives every slot's position
+// pos_s = s + max_{j<=s}(4 b_j - j) (slot indices stand in for ranks: the
+// offset of a clipped first chunk shifts every position equally).
+// Control words: [0] = c, [2] = dp; [4], [5] = plo.
+__device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ tgt, int64_t plo,
+                                        uint32_t dp, uint32_t c, uint32_t woff, int lane) {
+    const int64_t cs = (plo & ~(int64_t)3) + (int64_t)kChunk * c;  // chunk's first slot
+    const int64_t lo = max(cs, plo), hi = min(cs + (int64_t)kChunk, plo + (int64_t)dp);
+    const int64_t g0 = cs + 8 * lane;
+    uint4 ka = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty), kb = ka;
+    if (g0 < hi) ka = ldg(reinterpret_cast<const uint4 *>(tgt + g0));
+    if (g0 + 4 < hi) kb = ldg(reinterpret_cast<const uint4 *>(tgt + g0 + 4));
+    const uint32_t kmin = ldg(tgt + lo), kmax = ldg(tgt + hi - 1);
     __syncwarp();  // previous readers of the table are done
     uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + woff);
 #pragma unroll
@@ -507,27 +509,36 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ P, uint32_t
         if (x * 32 + lane < (int)(kTabSlots / 4))
             t4[x * 32 + lane] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     if (lane == 0) {
-        fw_smem[woff + kCtlWord + 0] = c0;
-        fw_smem[woff + kCtlWord + 1] = cn;
+        fw_smem[woff + kCtlWord + 0] = c;
         fw_smem[woff + kCtlWord + 2] = dp;
     }
     HashState hs;
-    hs.kmin = __shfl_sync(FULL, keys[0], 0);
-    const float range = (float)(kmax - hs.kmin) + 1.0f;
+    hs.kmin = kmin;
+    const float range = (float)(kmax - kmin) + 1.0f;
     hs.scale = (uint32_t)fminf(__fdividef((float)kGroups * 4294967296.0f, range), 4294967040.0f);
-    hs.lim = c0 + cn >= dp ? kEmpty : kmax;
-    __syncwarp();
-    int carry = INT_MIN;
+    hs.lim = cs + (int64_t)kChunk >= plo + (int64_t)dp ? kEmpty : kmax;
+    const uint32_t key[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+    const int s0 = 8 * lane;
+    const int vlo = (int)(lo - cs), vhi = (int)(hi - cs);  // valid slots [vlo, vhi)
+    int m[8];
+    int run = INT_MIN;
 #pragma unroll
-    for (int r = 0; r < kKeys; r++) {
-        const int i = r * 32 + lane;
-        const bool valid = (uint32_t)i < cn;
-        int v = valid ? (int)(4 * tab_group(keys[r], hs)) - i : INT_MIN;
+    for (int r = 0; r < 8; r++) {
+        const int sl = s0 + r;
+        const bool v = sl >= vlo && sl < vhi;
+        run = max(run, v ? (int)(4 * tab_group(key[r], hs)) - sl : INT_MIN);
+        m[r] = run;
+    }
+    int incl = run;  // inclusive max-scan over lanes (idempotent: no predicate)
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) v = max(v, __shfl_up_sync(FULL, v, d));  // idempotent
-        v = max(v, carry);
-        carry = __shfl_sync(FULL, v, 31);
-        if (valid) fw_smem[woff + i + v] = keys[r];
+    for (int d = 1; d < 32; d <<= 1) incl = max(incl, __shfl_up_sync(FULL, incl, d));
+    int excl = __shfl_up_sync(FULL, incl, 1);
+    if (lane == 0) excl = INT_MIN;
+    __syncwarp();  // the clear is complete
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const int sl = s0 + r;
+        if (sl >= vlo && sl < vhi) fw_smem[woff + sl + max(excl, m[r])] = key[r];
     }
     __syncwarp();
     return hs;
@@ -567,12 +578,17 @@ __device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ tgt, uint32
         for (int e = 3; e >= 0; e--)
             if ((need >> e) & 1) umin = u[e];
         umin = __reduce_min_sync(FULL, umin);
-        // advance: skip whole chunks that end below every pending u
-        const uint32_t *P = tgt + ctl_plo(woff);
+        // advance: skip whole chunks that end below every pending u (chunk
+        // c ends at slot A + 256c + 255; it is the last one when that
+        // reaches the end of N(prev))
+        const int64_t plo = ctl_plo(woff);
         const uint32_t dp = fw_smem[woff + kCtlWord + 2];
-        uint32_t c0 = fw_smem[woff + kCtlWord + 0] + fw_smem[woff + kCtlWord + 1];
-        while (c0 + kChunk < dp && ldg(P + c0 + kChunk - 1) < umin) c0 += kChunk;
-        hs = hash_build(P, c0, dp, woff, lane);
+        const int64_t end = plo + (int64_t)dp, A = plo & ~(int64_t)3;
+        uint32_t c = fw_smem[woff + kCtlWord + 0] + 1;
+        while (A + (int64_t)kChunk * (c + 1) < end &&
+               ldg(tgt + A + (int64_t)kChunk * c + kChunk - 1) < umin)
+            c++;
+        hs = hash_build(tgt, plo, dp, c, woff, lane);
         full = 0;
         uint32_t here = 0;
 #pragma unroll
@@ -702,7 +718,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(tp));
     stage_words(a, s, k, lane, woff, off);
     HashState hs{0, 0, 0};
-    if (use_hash) hs = hash_build(a.tgt + s.plo, 0, dp, woff, lane);
+    if (use_hash) hs = hash_build(a.tgt, s.plo, dp, 0, woff, lane);
     // counter of tile t: k == 256 -> t >> 1; k <= 128 -> t * (128 / k)
     const uint32_t cmul = k == 256 ? 0 : (128u >> (31 - __clz(k)));
     const uint32_t wq0 = (woff + kTabSlots) * 4 + 16 * lane;  // staged words (bytes)
@@ -872,7 +888,7 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         fw_smem[woff + kCtlWord + 5] = (uint32_t)((uint64_t)s.plo >> 32);
     }
     HashState hs{0, 0, 0};
-    if (use_hash) hs = hash_build(P, 0, dp, woff, lane);
+    if (use_hash) hs = hash_build(a.tgt, s.plo, dp, 0, woff, lane);
     else __syncwarp();
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;

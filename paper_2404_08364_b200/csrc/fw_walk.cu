@@ -26,6 +26,10 @@ namespace fw {
 // Cold helpers (window advance, hash build, binary-search fallback).
 // Inlined by default: an out-of-line call makes the tile loop save and
 // restore registers around it (measured 6.3e7 vs 5.4e7 steps/s).
+#ifndef FW_PREFETCH_CHUNK
+#define FW_PREFETCH_CHUNK 1
+#endif
+
 #ifndef FW_PREFILTER
 #define FW_PREFILTER 1
 #endif
@@ -502,6 +506,11 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ tgt, int64_
     if (g0 < hi) ka = ldg(reinterpret_cast<const uint4 *>(tgt + g0));
     if (g0 + 4 < hi) kb = ldg(reinterpret_cast<const uint4 *>(tgt + g0 + 4));
     const uint32_t kmin = ldg(tgt + lo), kmax = ldg(tgt + hi - 1);
+#if FW_PREFETCH_CHUNK
+    // the next chunk's slots into L1 (a window advance usually takes it next)
+    if (g0 + (int64_t)kChunk < plo + (int64_t)dp)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tgt + g0 + kChunk));
+#endif
     __syncwarp();  // previous readers of the table are done
     uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + woff);
 #pragma unroll

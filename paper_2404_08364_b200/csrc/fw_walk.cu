@@ -497,46 +497,80 @@ __device__ __forceinline__ bool bucket_has(const uint4 q, uint32_t u) {
 // pos_s = s + max_{j<=s}(4 b_j - j) (slot indices stand in for ranks: the
 // offset of a clipped first chunk shifts every position equally).
 // Control words: [0] = c, [2] = dp; [4], [5] = plo.
-__device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ tgt, int64_t plo,
-                                        uint32_t dp, uint32_t c, uint32_t woff, int lane) {
-    const int64_t cs = (plo & ~(int64_t)3) + (int64_t)kChunk * c;  // chunk's first slot
-    const int64_t lo = max(cs, plo), hi = min(cs + (int64_t)kChunk, plo + (int64_t)dp);
-    const int64_t g0 = cs + 8 * lane;
-    uint4 ka = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty), kb = ka;
-    if (g0 < hi) ka = ldg(reinterpret_cast<const uint4 *>(tgt + g0));
-    if (g0 + 4 < hi) kb = ldg(reinterpret_cast<const uint4 *>(tgt + g0 + 4));
-    const uint32_t kmin = ldg(tgt + lo), kmax = ldg(tgt + hi - 1);
-#if FW_PREFETCH_CHUNK
-    // the next chunk's slots into L1 (a window advance usually takes it next)
-    if (g0 + (int64_t)kChunk < plo + (int64_t)dp)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(tgt + g0 + kChunk));
-#endif
-    __syncwarp();  // previous readers of the table are done
+__device__ __forceinline__ void tab_clear(uint32_t woff, int lane) {
     uint4 *t4 = reinterpret_cast<uint4 *>(fw_smem + woff);
 #pragma unroll
     for (int x = 0; x < (int)((kTabSlots / 4 + 31) / 32); x++)
         if (x * 32 + lane < (int)(kTabSlots / 4))
             t4[x * 32 + lane] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+}
+
+__device__ __forceinline__ uint32_t tab_scale(uint32_t kmin, uint32_t kmax) {
+    const float range = (float)(kmax - kmin) + 1.0f;
+    return (uint32_t)fminf(__fdividef((float)kGroups * 4294967296.0f, range), 4294967040.0f);
+}
+
+__device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ tgt, int64_t plo,
+                                        uint32_t dp, uint32_t c, uint32_t woff, int lane) {
+    const int64_t end = plo + (int64_t)dp;
+    const int64_t cs = (plo & ~(int64_t)3) + (int64_t)kChunk * c;  // chunk's first slot
+    const uint32_t *cp = tgt + cs;
+    const int s0 = 8 * lane;
+    HashState hs;
+    uint32_t key[8];
+    int m[8];
+    int run = INT_MIN;
+    if (cs >= plo && cs + (int64_t)kChunk <= end) {
+        // whole chunk inside N(prev) (the common case): no per-slot checks
+        const uint4 ka = ldg(reinterpret_cast<const uint4 *>(cp + s0));
+        const uint4 kb = ldg(reinterpret_cast<const uint4 *>(cp + s0 + 4));
+#if FW_PREFETCH_CHUNK
+        if (cs + 2 * (int64_t)kChunk <= end)  // the next chunk into L1
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(cp + kChunk + s0));
+#endif
+        key[0] = ka.x; key[1] = ka.y; key[2] = ka.z; key[3] = ka.w;
+        key[4] = kb.x; key[5] = kb.y; key[6] = kb.z; key[7] = kb.w;
+        hs.kmin = __shfl_sync(FULL, key[0], 0);
+        const uint32_t kmax = __shfl_sync(FULL, key[7], 31);
+        hs.scale = tab_scale(hs.kmin, kmax);
+        hs.lim = cs + (int64_t)kChunk >= end ? kEmpty : kmax;
+        __syncwarp();  // previous readers of the table are done
+        tab_clear(woff, lane);
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            run = max(run, (int)(4 * tab_group(key[r], hs)) - (s0 + r));
+            m[r] = run;
+        }
+    } else {
+        const int64_t lo = max(cs, plo), hi = min(cs + (int64_t)kChunk, end);
+        const int64_t g0 = cs + s0;
+        uint4 ka = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty), kb = ka;
+        if (g0 < hi) ka = ldg(reinterpret_cast<const uint4 *>(tgt + g0));
+        if (g0 + 4 < hi) kb = ldg(reinterpret_cast<const uint4 *>(tgt + g0 + 4));
+        hs.kmin = ldg(tgt + lo);
+        const uint32_t kmax = ldg(tgt + hi - 1);
+#if FW_PREFETCH_CHUNK
+        if (g0 + (int64_t)kChunk < end)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tgt + g0 + kChunk));
+#endif
+        key[0] = ka.x; key[1] = ka.y; key[2] = ka.z; key[3] = ka.w;
+        key[4] = kb.x; key[5] = kb.y; key[6] = kb.z; key[7] = kb.w;
+        hs.scale = tab_scale(hs.kmin, kmax);
+        hs.lim = cs + (int64_t)kChunk >= end ? kEmpty : kmax;
+        __syncwarp();  // previous readers of the table are done
+        tab_clear(woff, lane);
+        const int vlo = (int)(lo - cs), vhi = (int)(hi - cs);  // valid slots [vlo, vhi)
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int sl = s0 + r;
+            const bool v = sl >= vlo && sl < vhi;
+            run = max(run, v ? (int)(4 * tab_group(key[r], hs)) - sl : INT_MIN);
+            m[r] = v ? run : INT_MAX;  // INT_MAX marks an invalid slot
+        }
+    }
     if (lane == 0) {
         fw_smem[woff + kCtlWord + 0] = c;
         fw_smem[woff + kCtlWord + 2] = dp;
-    }
-    HashState hs;
-    hs.kmin = kmin;
-    const float range = (float)(kmax - kmin) + 1.0f;
-    hs.scale = (uint32_t)fminf(__fdividef((float)kGroups * 4294967296.0f, range), 4294967040.0f);
-    hs.lim = cs + (int64_t)kChunk >= plo + (int64_t)dp ? kEmpty : kmax;
-    const uint32_t key[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
-    const int s0 = 8 * lane;
-    const int vlo = (int)(lo - cs), vhi = (int)(hi - cs);  // valid slots [vlo, vhi)
-    int m[8];
-    int run = INT_MIN;
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-        const int sl = s0 + r;
-        const bool v = sl >= vlo && sl < vhi;
-        run = max(run, v ? (int)(4 * tab_group(key[r], hs)) - sl : INT_MIN);
-        m[r] = run;
     }
     int incl = run;  // inclusive max-scan over lanes (idempotent: no predicate)
 #pragma unroll
@@ -545,10 +579,8 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ tgt, int64_
     if (lane == 0) excl = INT_MIN;
     __syncwarp();  // the clear is complete
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
-        const int sl = s0 + r;
-        if (sl >= vlo && sl < vhi) fw_smem[woff + sl + max(excl, m[r])] = key[r];
-    }
+    for (int r = 0; r < 8; r++)
+        if (m[r] != INT_MAX) fw_smem[woff + s0 + r + max(excl, m[r])] = key[r];
     __syncwarp();
     return hs;
 }

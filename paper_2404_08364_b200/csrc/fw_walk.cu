@@ -510,26 +510,57 @@ __device__ __forceinline__ uint32_t tab_scale(uint32_t kmin, uint32_t kmax) {
     return (uint32_t)fminf(__fdividef((float)kGroups * 4294967296.0f, range), 4294967040.0f);
 }
 
-__device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ tgt, int64_t plo,
-                                        uint32_t dp, uint32_t c, uint32_t woff, int lane) {
+// The keys of chunk c, loaded ahead of the build so the load latency can
+// overlap other work (the step prologue issues them before staging the draw
+// words).
+struct ChunkKeys {
+    uint4 ka, kb;
+    uint32_t kmin, kmax;
+};
+
+__device__ __forceinline__ ChunkKeys chunk_load(const uint32_t *__restrict__ tgt, int64_t plo,
+                                                uint32_t dp, uint32_t c, int lane) {
     const int64_t end = plo + (int64_t)dp;
     const int64_t cs = (plo & ~(int64_t)3) + (int64_t)kChunk * c;  // chunk's first slot
-    const uint32_t *cp = tgt + cs;
     const int s0 = 8 * lane;
+    ChunkKeys ck;
+    if (cs >= plo && cs + (int64_t)kChunk <= end) {
+        // whole chunk inside N(prev) (the common case): min/max come by shuffle
+        ck.ka = ldg(reinterpret_cast<const uint4 *>(tgt + cs + s0));
+        ck.kb = ldg(reinterpret_cast<const uint4 *>(tgt + cs + s0 + 4));
+        ck.kmin = ck.kmax = 0;
+#if FW_PREFETCH_CHUNK
+        if (cs + 2 * (int64_t)kChunk <= end)  // the next chunk into L1
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tgt + cs + kChunk + s0));
+#endif
+    } else {
+        const int64_t lo = max(cs, plo), hi = min(cs + (int64_t)kChunk, end);
+        const int64_t g0 = cs + s0;
+        ck.ka = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        ck.kb = ck.ka;
+        if (g0 < hi) ck.ka = ldg(reinterpret_cast<const uint4 *>(tgt + g0));
+        if (g0 + 4 < hi) ck.kb = ldg(reinterpret_cast<const uint4 *>(tgt + g0 + 4));
+        ck.kmin = ldg(tgt + lo);
+        ck.kmax = ldg(tgt + hi - 1);
+#if FW_PREFETCH_CHUNK
+        if (g0 + (int64_t)kChunk < end)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tgt + g0 + kChunk));
+#endif
+    }
+    return ck;
+}
+
+__device__ FW_COLD HashState hash_build(const ChunkKeys &ck, int64_t plo, uint32_t dp,
+                                        uint32_t c, uint32_t woff, int lane) {
+    const int64_t end = plo + (int64_t)dp;
+    const int64_t cs = (plo & ~(int64_t)3) + (int64_t)kChunk * c;
+    const int s0 = 8 * lane;
+    const uint32_t key[8] = {ck.ka.x, ck.ka.y, ck.ka.z, ck.ka.w,
+                             ck.kb.x, ck.kb.y, ck.kb.z, ck.kb.w};
     HashState hs;
-    uint32_t key[8];
     int m[8];
     int run = INT_MIN;
     if (cs >= plo && cs + (int64_t)kChunk <= end) {
-        // whole chunk inside N(prev) (the common case): no per-slot checks
-        const uint4 ka = ldg(reinterpret_cast<const uint4 *>(cp + s0));
-        const uint4 kb = ldg(reinterpret_cast<const uint4 *>(cp + s0 + 4));
-#if FW_PREFETCH_CHUNK
-        if (cs + 2 * (int64_t)kChunk <= end)  // the next chunk into L1
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(cp + kChunk + s0));
-#endif
-        key[0] = ka.x; key[1] = ka.y; key[2] = ka.z; key[3] = ka.w;
-        key[4] = kb.x; key[5] = kb.y; key[6] = kb.z; key[7] = kb.w;
         hs.kmin = __shfl_sync(FULL, key[0], 0);
         const uint32_t kmax = __shfl_sync(FULL, key[7], 31);
         hs.scale = tab_scale(hs.kmin, kmax);
@@ -543,20 +574,9 @@ __device__ FW_COLD HashState hash_build(const uint32_t *__restrict__ tgt, int64_
         }
     } else {
         const int64_t lo = max(cs, plo), hi = min(cs + (int64_t)kChunk, end);
-        const int64_t g0 = cs + s0;
-        uint4 ka = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty), kb = ka;
-        if (g0 < hi) ka = ldg(reinterpret_cast<const uint4 *>(tgt + g0));
-        if (g0 + 4 < hi) kb = ldg(reinterpret_cast<const uint4 *>(tgt + g0 + 4));
-        hs.kmin = ldg(tgt + lo);
-        const uint32_t kmax = ldg(tgt + hi - 1);
-#if FW_PREFETCH_CHUNK
-        if (g0 + (int64_t)kChunk < end)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(tgt + g0 + kChunk));
-#endif
-        key[0] = ka.x; key[1] = ka.y; key[2] = ka.z; key[3] = ka.w;
-        key[4] = kb.x; key[5] = kb.y; key[6] = kb.z; key[7] = kb.w;
-        hs.scale = tab_scale(hs.kmin, kmax);
-        hs.lim = cs + (int64_t)kChunk >= end ? kEmpty : kmax;
+        hs.kmin = ck.kmin;
+        hs.scale = tab_scale(ck.kmin, ck.kmax);
+        hs.lim = cs + (int64_t)kChunk >= end ? kEmpty : ck.kmax;
         __syncwarp();  // previous readers of the table are done
         tab_clear(woff, lane);
         const int vlo = (int)(lo - cs), vhi = (int)(hi - cs);  // valid slots [vlo, vhi)
@@ -629,7 +649,7 @@ __device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ tgt, uint32
         while (A + (int64_t)kChunk * (c + 1) < end &&
                ldg(tgt + A + (int64_t)kChunk * c + kChunk - 1) < umin)
             c++;
-        hs = hash_build(tgt, plo, dp, c, woff, lane);
+        hs = hash_build(chunk_load(tgt, plo, dp, c, lane), plo, dp, c, woff, lane);
         full = 0;
         uint32_t here = 0;
 #pragma unroll
@@ -757,9 +777,11 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     // round trips of a step's prologue overlap
     uint4 nu = make_uint4(0, 0, 0, 0);
     if ((uint32_t)lane * 4 < span) nu = ldg(reinterpret_cast<const uint4 *>(tp));
-    stage_words(a, s, k, lane, woff, off);
+    ChunkKeys ck0{};
+    if (use_hash) ck0 = chunk_load(a.tgt, s.plo, dp, 0, lane);
+    stage_words(a, s, k, lane, woff, off);  // overlaps the loads above
     HashState hs{0, 0, 0};
-    if (use_hash) hs = hash_build(a.tgt, s.plo, dp, 0, woff, lane);
+    if (use_hash) hs = hash_build(ck0, s.plo, dp, 0, woff, lane);
     // counter of tile t: k == 256 -> t >> 1; k <= 128 -> t * (128 / k)
     const uint32_t cmul = k == 256 ? 0 : (128u >> (31 - __clz(k)));
     const uint32_t wq0 = (woff + kTabSlots) * 4 + 16 * lane;  // staged words (bytes)
@@ -929,7 +951,7 @@ __device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t
         fw_smem[woff + kCtlWord + 5] = (uint32_t)((uint64_t)s.plo >> 32);
     }
     HashState hs{0, 0, 0};
-    if (use_hash) hs = hash_build(a.tgt, s.plo, dp, 0, woff, lane);
+    if (use_hash) hs = hash_build(chunk_load(a.tgt, s.plo, dp, 0, lane), s.plo, dp, 0, woff, lane);
     else __syncwarp();
     double carry = 0.0;
     uint32_t cand = 0, cand_u = 0;

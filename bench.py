@@ -10,7 +10,8 @@ mode, seed 0.  A "step" is one pass of the walk kernel over all V queries.
                ranks; graph + result pool (1.9 GB) exceed L2, so no flush.
   e2e          the same metric through the C-ABI host-buffer call fw_walk
                (H2D of the starts from pinned memory, D2H of sequences+lengths
-               into pinned memory inside the timed region).
+               into pinned memory inside the timed region; fw_walk copies the
+               result back in 16 pieces, each as soon as its queries finish).
   roofline     algorithmic bytes per launch / mean launch time vs
                the measured HBM copy bandwidth (MEASURED_PEAKS.json).
   cpu_baseline the reference itself (baseline/_ref reswalk, numba, all host
@@ -428,7 +429,8 @@ def bench_ours(args):
             dist.all_reduce(e2e_tot, op=dist.ReduceOp.SUM)
         e2e = {"value": int(e2e_tot.item()) / float(e2e_s.item()), "unit": "steps/s",
                "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * L * 4 + n * 4,
-               "path": "fw_walk (C ABI, pinned host buffers)"}
+               "path": "fw_walk (C ABI, pinned host buffers)",
+               "d2h_pieces_overlapped": int(fst.d2h_pieces)}
         del hseq
 
     peak, peak_kind = measured_peak()

@@ -91,7 +91,8 @@ typedef struct {
     int32_t exact_order;    /* 1 if tree-order scans were used */
     int32_t grid_ctas;
     int32_t kernel_launches;
-    int32_t reserved;
+    int32_t d2h_pieces;     /* fw_walk: result pieces copied back while the walk ran
+                               (0: copied after the kernel) */
     double tail_ms;         /* first to last warp exit: the load-imbalance tail */
 } fw_stats;
 

@@ -37,7 +37,7 @@ class FwStats(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in ST_FIELDS] + [
         ("kernel_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
         ("exact_order", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
-        ("kernel_launches", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32), ("d2h_pieces", ctypes.c_int32),
         ("tail_ms", ctypes.c_double)]
 
 

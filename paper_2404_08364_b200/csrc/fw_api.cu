@@ -1,6 +1,7 @@
 // C ABI of libflowwalk.so (declared in include/flowwalk.h): device-resident
 // CSR handle, walk launch (device and host buffers), GPU validator and the
 // synthetic-input generators.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -77,7 +78,7 @@ struct fw_graph {
     std::mutex mu;
     std::mutex host_mu;  // serialises fw_walk's host-buffer scratch
     // host-buffer walk scratch (grow-only)
-    DevBuf starts, seq, len, stats, schema;
+    DevBuf starts, seq, len, stats, schema, done;
     std::vector<DevBuf> schema_ring;
     int sm_count = 0;
 };
@@ -281,6 +282,7 @@ extern "C" int fw_graph_destroy(fw_graph *g) {
     g->len.release();
     g->stats.release();
     g->schema.release();
+    g->done.release();
     for (auto &b : g->schema_ring) b.release();
     delete g;
     return FW_OK;
@@ -352,7 +354,7 @@ static int check_cfg(fw_graph *g, const fw_app *app, const fw_engine *eng) {
 static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t base_qid,
                   const fw_app *app, const fw_engine *eng, uint64_t seed, uint32_t *d_seq,
                   uint32_t *d_len, int64_t *d_stats, cudaStream_t stream, bool *exact_out,
-                  int *grid_out) {
+                  int *grid_out, unsigned *d_done = nullptr, uint64_t piece_q = 0) {
     if (base_qid + n > (1ull << 33))
         return set_err(FW_ECONFIG, "query ids exceed the replay stream-id field (2^33)");
     const bool exact = eng->order_mode == FW_ORDER_AUTO && exact_order_ok(g->info, *app);
@@ -416,6 +418,8 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         a.merge_ratio = mr ? (uint32_t)atoi(mr) : 32u;
     }
     a.stats = (long long *)d_stats;
+    a.done = d_done;
+    a.piece_q = piece_q ? piece_q : 1;
     unsigned slot;
     {
         std::lock_guard<std::mutex> lk(g->mu);
@@ -453,6 +457,28 @@ extern "C" int fw_walk_device(fw_graph *g, const int64_t *d_starts, uint64_t n,
                   (cudaStream_t)stream, nullptr, nullptr);
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point (no link-time
+// dependency on libcuda); null when the driver does not provide it or
+// FW_D2H_OVERLAP=0.
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValue32Fn wait_value32() {
+    static WaitValue32Fn fn = [] {
+        const char *env = getenv("FW_D2H_OVERLAP");
+        if (env && env[0] == '0') return (WaitValue32Fn) nullptr;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault,
+                                             &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (WaitValue32Fn) nullptr;
+        return (WaitValue32Fn)p;
+    }();
+    return fn;
+}
+
+constexpr uint64_t kD2hPieces = 16;         // result pieces for the overlapped D2H
+constexpr uint64_t kD2hMinQueries = 65536;  // below this, copy after the walk
+
 extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t base_qid,
                        const fw_app *app, const fw_engine *eng, uint64_t seed,
                        uint32_t *out_seq, uint32_t *out_len, fw_stats *stats) {
@@ -465,33 +491,69 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     CU(g->seq.reserve(std::max<uint64_t>(n * L, 1) * sizeof(uint32_t)));
     CU(g->len.reserve(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
     CU(g->stats.reserve(ST_WORDS * sizeof(int64_t)));
-    cudaStream_t st;
+    // Pieces of the result are copied back on a second stream as soon as all
+    // of a piece's queries are done (the kernel counts them; the copy stream
+    // waits on the count), so only the last piece's D2H trails the walk.
+    WaitValue32Fn wv = n >= kD2hMinQueries ? wait_value32() : nullptr;
+    const uint64_t P = wv ? kD2hPieces : 0;
+    const uint64_t piece_q = P ? (n + P - 1) / P : 0;
+    if (P) CU(g->done.reserve(P * sizeof(unsigned)));
+    cudaStream_t st, cs;
     CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    cudaEvent_t e0, e1, e2, e3;
+    CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1, e2, e3, ez;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventCreate(&e2);
     cudaEventCreate(&e3);
+    cudaEventCreateWithFlags(&ez, cudaEventDisableTiming);
     cudaEventRecord(e0, st);
     cudaMemsetAsync(g->stats.p, 0, ST_WORDS * sizeof(int64_t), st);
+    if (P) cudaMemsetAsync(g->done.p, 0, P * sizeof(unsigned), st);
     if (n) cudaMemcpyAsync(g->starts.p, starts, n * sizeof(int64_t), cudaMemcpyHostToDevice, st);
     cudaEventRecord(e1, st);
+    cudaEventRecord(ez, st);  // the counters are zero from here on
     bool exact = false;
     int grid = 0;
     rc = launch(g, (const int64_t *)g->starts.p, n, base_qid, app, eng, seed,
                 (uint32_t *)g->seq.p, (uint32_t *)g->len.p, (int64_t *)g->stats.p, st, &exact,
-                &grid);
+                &grid, P ? (unsigned *)g->done.p : nullptr, piece_q);
     cudaEventRecord(e2, st);
     int64_t hst[ST_WORDS] = {0};
+    int pieces = 0;
     if (!rc) {
-        if (n) {
+        if (P) {
+            cudaStreamWaitEvent(cs, ez, 0);
+            for (uint64_t i = 0; i < P && i * piece_q < n; i++) {
+                const uint64_t q0 = i * piece_q, cnt = std::min(piece_q, n - q0);
+                const CUdeviceptr dc = (CUdeviceptr)((unsigned *)g->done.p + i);
+                if (wv(cs, dc, (cuuint32_t)cnt, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+                    rc = set_err(FW_ECUDA, "cuStreamWaitValue32 failed");
+                    break;
+                }
+                cudaMemcpyAsync(out_seq + q0 * L, (uint32_t *)g->seq.p + q0 * L,
+                                cnt * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, cs);
+                cudaMemcpyAsync(out_len + q0, (uint32_t *)g->len.p + q0, cnt * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, cs);
+                pieces++;
+            }
+            cudaStreamWaitEvent(st, e2, 0);
+        } else if (n) {
             cudaMemcpyAsync(out_seq, g->seq.p, n * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
             cudaMemcpyAsync(out_len, g->len.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
         }
         cudaMemcpyAsync(hst, g->stats.p, sizeof(hst), cudaMemcpyDeviceToHost, st);
+        if (P) {  // the end event covers both streams
+            cudaEvent_t ec;
+            cudaEventCreateWithFlags(&ec, cudaEventDisableTiming);
+            cudaEventRecord(ec, cs);
+            cudaStreamWaitEvent(st, ec, 0);
+            cudaEventDestroy(ec);
+        }
         cudaEventRecord(e3, st);
         cudaError_t ce = cudaStreamSynchronize(st);
-        if (ce != cudaSuccess)
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(cs);
+        if (ce != cudaSuccess && !rc)
             rc = set_err(FW_ECUDA, "walk failed: %s", cudaGetErrorString(ce));
     }
     if (!rc && stats) {
@@ -511,6 +573,7 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         stats->exact_order = exact;
         stats->grid_ctas = grid;
         stats->kernel_launches = n ? 1 : 0;
+        stats->d2h_pieces = pieces;
         const uint64_t last = (uint64_t)hst[ST_T_LAST], first = ~(uint64_t)hst[ST_T_FIRST_NEG];
         stats->tail_ms = (n && last >= first) ? (double)(last - first) * 1e-6 : 0.0;
     }
@@ -518,7 +581,9 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     cudaEventDestroy(e3);
+    cudaEventDestroy(ez);
     cudaStreamDestroy(st);
+    cudaStreamDestroy(cs);
     return rc;
 }
 

@@ -1171,6 +1171,11 @@ walk_kernel(const WalkArgs a) {
             pathbuf = 0xFFFFFFFFu;
         }
         if (lane == 0) a.out_len[qi] = emitted;
+        if (a.done) {  // publish the finished row for the overlapped D2H
+            __threadfence_system();
+            __syncwarp();
+            if (lane == 0) atomicAdd(a.done + qi / a.piece_q, 1u);
+        }
         stat_add(st, ST_SAMPLED, emitted, lane);
     }
     if (lane == 0) {

@@ -60,6 +60,12 @@ struct WalkArgs {
     // fp32 for every weight, so factor * weight is formed in fp32 and widened
     int32_t fac32;
     float inv_a32, inv_b32;
+    // per-piece completion counters (null: off).  A warp that finishes
+    // query qi bumps done[qi / piece_q] after a system-scope fence, so the
+    // host's copy stream can wait on a piece (cuStreamWaitValue32) and copy
+    // its paths back while the walk continues.
+    unsigned *done;
+    uint64_t piece_q;
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };

@@ -324,3 +324,32 @@ def test_deepwalk_one_step_distribution_chi_square():
                          minlength=len(uniq)).astype(np.float64)
     passed, stat, dof = _chi2_pass(counts, p_u)
     assert passed, (stat, dof)
+
+
+def test_overlapped_d2h_pieces_bit_exact(s16):
+    """fw_walk copies the result back in 16 pieces while the walk runs (each
+    piece waits on the kernel's per-piece completion counter); the host
+    arrays must equal the oracle's, bit for bit."""
+    from paper_2404_08364_b200 import _lib, engine
+    g = s16
+    starts = np.arange(g.vertex_count, dtype=np.int64)
+    app_cfg = fw.AppConfig(app="node2vec", length=40, a=2.0, b=0.5)
+    eng_cfg = fw.EngineConfig(replay=True)
+    app, eng, _schema = engine._fw_structs(app_cfg, eng_cfg)
+    sess = engine._Session(g, eng_cfg)
+    try:
+        seq = np.full(len(starts) * app_cfg.length, 7, np.uint32)
+        ln = np.full(len(starts), 7, np.uint32)
+        st = _lib.FwStats()
+        lib = _lib.load()
+        rc = lib.fw_walk(sess.handles[0].ptr, starts.ctypes.data, len(starts), 0,
+                         engine._ctypes_ref(app), engine._ctypes_ref(eng), 5,
+                         seq.ctypes.data, ln.ctypes.data, engine._ctypes_ref(st))
+        _lib.check(rc)
+    finally:
+        sess.close()
+    assert st.d2h_pieces == 16 and st.kernel_launches == 1
+    oseq, oln, _ = oracle.walk(g.offsets, g.targets, g.weights, g.labels, starts,
+                               app="node2vec", length=40, a=2.0, b=0.5, seed=5)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq.reshape(len(starts), -1), oseq)

@@ -825,7 +825,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             // lookups for every slot (prev's and invalid slots' results are
             // ignored); the cold path handles valid slots beyond the window
             // and those in a full group whose last key is < u
-            uint32_t full = 0, pend = 0;
+            uint32_t full = 0;
 #pragma unroll
             for (int e = 0; e < 4; e++) {
                 const uint4 q = bucket_at(woff, tab_group(u[e], hs));
@@ -836,11 +836,21 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                     mem |= (hit ? 1u : 0u) << e;
                 }
                 full |= (!hit && q.w < u[e] ? 1u : 0u) << e;
-                pend |= (u[e] > hs.lim ? 1u : 0u) << e;
             }
-            pend &= valid;
-            full &= valid & ~pend;
-            if (__any_sync(FULL, full | pend)) {
+            // a valid slot beyond the window: u is sorted within the lane, so
+            // in an interior tile u[3] decides
+            bool beyond = !edge && u[3] > hs.lim;
+            if (edge) {
+#pragma unroll
+                for (int e = 0; e < 4; e++) beyond |= ((valid >> e) & 1) && u[e] > hs.lim;
+            }
+            full &= valid;
+            if (__any_sync(FULL, full || beyond)) {
+                uint32_t pend = 0;
+#pragma unroll
+                for (int e = 0; e < 4; e++) pend |= (u[e] > hs.lim ? 1u : 0u) << e;
+                pend &= valid;
+                full &= ~pend;
                 const SlowRet sr =
                     member4_slow(a.tgt, woff, u[0], u[1], u[2], u[3], full, pend, hs, lane);
                 hs = sr.hs;

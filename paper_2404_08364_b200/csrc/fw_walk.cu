@@ -786,7 +786,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     const uint32_t cmul = k == 256 ? 0 : (128u >> (31 - __clz(k)));
     const uint32_t wq0 = (woff + kTabSlots) * 4 + 16 * lane;  // staged words (bytes)
     double carry = 0.0;
-    uint32_t cand = 0, cand_u = 0;
+    uint32_t cand = 0;
     const uint32_t ntiles = (span + 127) >> 7;
     for (uint32_t t = 0; t < ntiles; t++, tp += 128) {
         const uint32_t x0 = t * 128;  // first slot of the tile
@@ -916,7 +916,6 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                     const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
                     if (wv[e] > 0.0 && Pr < wv[e]) {
                         cand = (uint32_t)(i0 + e) + 1;
-                        cand_u = u[e];
                     }
                 }
             }
@@ -928,14 +927,13 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
             if (wv[e] > 0.0 && Pr < wv[e]) {
                 cand = (uint32_t)(i0 + e) + 1;
-                cand_u = u[e];
             }
         }
 #endif
     }
+    // the selected target is reloaded by the caller (L1/L2-resident): not
+    // carrying it frees the u registers before the draws
     const uint32_t sel = __reduce_max_sync(FULL, cand);
-    const unsigned who = __ballot_sync(FULL, cand == sel);
-    sel_u = __shfl_sync(FULL, cand_u, __ffs(who) - 1);
     __syncwarp();  // the table and the staged words are rebuilt by the next step
     return sel;
 }
@@ -1134,12 +1132,13 @@ walk_kernel(const WalkArgs a) {
             if constexpr (SAMPLER == SAMPLER_DPRS) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
-                        if (k >= 4 && k <= 256 && (k & (k - 1)) == 0)
+                        if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
                             sel = a.fac32 ? dprs_n2v_pow2<true>(a, s, k, lane, woff, sel_u)
                                           : dprs_n2v_pow2<false>(a, s, k, lane, woff, sel_u);
-                        else
+                        } else {
                             sel = dprs_n2v_exact<0>(a, s, k, lane, woff, sel_u);
-                        have_u = true;
+                            have_u = true;
+                        }
                     } else {
                         sel = dprs_warp_exact<APP>(a, s, k, lane);
                     }

@@ -895,7 +895,6 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                                 (((uint64_t)qa.w << 32) | qa.z) + cg,
                                 (((uint64_t)qb.y << 32) | qb.x) + cg,
                                 (((uint64_t)qb.w << 32) | qb.z) + cg};
-        const double pre[4] = {wv[0], p1, p2, p3};
 #if FW_PREFILTER
         // Accept prefilter.  Element e is accepted iff w > 0 and fl(r*P) < w
         // with P = base + pre[e] >= base + w, which implies r < w/(base + w)
@@ -909,18 +908,22 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
 #pragma unroll
         for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;
         if (pass & valid) {
+            // P = base + w_0 + ... + w_e, recomputed here (every partial sum
+            // is exact, so the association order does not matter) so that
+            // only the fp32 products stay live across the draws
+            double run = base;
 #pragma unroll
             for (int e = 0; e < 4; e++) {
+                const double w = F32 ? (double)wp[e] : wv[e];
+                run = __dadd_rn(run, w);
                 if ((pass >> e) & 1) {
                     const double r = u01_word(wd[e]);
-                    const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
-                    if (wv[e] > 0.0 && Pr < wv[e]) {
-                        cand = (uint32_t)(i0 + e) + 1;
-                    }
+                    if (w > 0.0 && __dmul_rn(r, run) < w) cand = (uint32_t)(i0 + e) + 1;
                 }
             }
         }
 #else
+        const double pre[4] = {wv[0], p1, p2, p3};
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const double r = u01_word(wd[e]);

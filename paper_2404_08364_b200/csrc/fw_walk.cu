@@ -473,7 +473,7 @@ __device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
 // loop (kmin, scale, lim = kmax or ~0 for the last chunk); chunk start,
 // length and d(prev) sit in the warp's control words (kCtlWord).
 constexpr uint32_t kGroups = 304;
-static_assert(4 * (kGroups - 1) + kChunk <= kTabSlots, "table overflow");
+static_assert(4 * (kGroups - 1) + kChunk < kTabSlots, "table overflow (the last slot is the dump)");
 
 struct HashState {
     uint32_t kmin, scale, lim;
@@ -598,9 +598,14 @@ __device__ FW_COLD HashState hash_build(const ChunkKeys &ck, int64_t plo, uint32
     int excl = __shfl_up_sync(FULL, incl, 1);
     if (lane == 0) excl = INT_MIN;
     __syncwarp();  // the clear is complete
+    // unconditional stores (no per-key branches): an invalid slot writes
+    // kEmpty to the table's last slot, which no key ever occupies (positions
+    // stay below 4 (kGroups - 1) + kChunk), so it reads as empty
 #pragma unroll
-    for (int r = 0; r < 8; r++)
-        if (m[r] != INT_MAX) fw_smem[woff + s0 + r + max(excl, m[r])] = key[r];
+    for (int r = 0; r < 8; r++) {
+        const bool v = m[r] != INT_MAX;
+        fw_smem[woff + (v ? s0 + r + max(excl, m[r]) : kTabSlots - 1)] = v ? key[r] : kEmpty;
+    }
     __syncwarp();
     return hs;
 }

@@ -658,14 +658,17 @@ __device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ tgt, uint32
         full = 0;
         uint32_t here = 0;
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-            if (((need >> e) & 1) && u[e] <= hs.lim) {
-                here |= 1u << e;
-                const uint4 q = bucket_at(woff, tab_group(u[e], hs));
-                if (bucket_has(q, u[e])) mem |= 1u << e;
-                else if (q.w < u[e]) full |= 1u << e;
-            }
+        for (int e = 0; e < 4; e++) {  // branch-free re-lookups, masked after
+            const uint4 q = bucket_at(woff, tab_group(u[e], hs));
+            const bool hit = bucket_has(q, u[e]);
+            here |= (u[e] <= hs.lim ? 1u : 0u) << e;
+            mem |= (hit ? 1u : 0u) << e;
+            full |= (!hit && q.w < u[e] ? 1u : 0u) << e;
         }
+        // a hit for a slot that was not pending is a true member found
+        // earlier (an older window's keys all lie below this window's)
+        here &= need;
+        full &= here;
         need &= ~here;
     }
 }

@@ -651,10 +651,14 @@ __device__ FW_COLD SlowRet member4_slow(const uint32_t *__restrict__ tgt, uint32
         const uint32_t dp = fw_smem[woff + kCtlWord + 2];
         const int64_t end = plo + (int64_t)dp, A = plo & ~(int64_t)3;
         uint32_t c = fw_smem[woff + kCtlWord + 0] + 1;
+        ChunkKeys ck = chunk_load(tgt, plo, dp, c, lane);
+        // the loaded chunk's own max decides a skip (no separate probe load)
         while (A + (int64_t)kChunk * (c + 1) < end &&
-               ldg(tgt + A + (int64_t)kChunk * c + kChunk - 1) < umin)
+               __shfl_sync(FULL, ck.kb.w, 31) < umin) {
             c++;
-        hs = hash_build(chunk_load(tgt, plo, dp, c, lane), plo, dp, c, woff, lane);
+            ck = chunk_load(tgt, plo, dp, c, lane);
+        }
+        hs = hash_build(ck, plo, dp, c, woff, lane);
         full = 0;
         uint32_t here = 0;
 #pragma unroll

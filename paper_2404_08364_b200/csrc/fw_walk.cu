@@ -386,22 +386,23 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
 //
 // Layout: tiles of 128 elements of N(cur), lane p holding 4 consecutive
 // elements (16-byte loads of targets and weights; the tile grid is anchored
-// at elo & ~3 and out-of-range slots are masked), so the natural-order fp64
-// prefix is a 4-element local prefix plus one warp scan per 128 elements.
-// The next tile is loaded while the current one is processed.
+// at elo & ~3 and only the first and last tiles mask slots), so the
+// natural-order fp64 prefix is a 4-element local prefix plus one warp scan
+// per 128 elements.  The next tile's targets are loaded one tile ahead.
 //
 // Membership u in N(prev) (_kernels.py:288-306): N(prev) is sorted and the
-// u values only grow along N(cur), so N(prev) is consumed in chunks of up to
-// kChunk entries, each hashed into a per-warp open-addressing table in
-// shared memory; a lane looks u up when u <= max(chunk) (or the chunk is the
-// last one), otherwise the window advances (skipping chunks whose max is
-// below every pending u).  N(prev) is read once, coalesced.  When d(prev) is
-// far larger than d(cur) a per-element branchless binary search in global
-// memory is cheaper and is used instead.
+// u values only grow along N(cur), so N(prev) is consumed in windows of
+// kChunk slots, each stored in an order-preserving hashed sorted table in
+// the warp's shared memory (hash_build, below); a lane looks u up when u <=
+// max(window) (or the window is the last one), otherwise the window advances
+// (skipping windows whose max is below every pending u).  N(prev) is read
+// once, coalesced.  When d(prev) is far larger than d(cur) a per-element
+// branchless binary search in global memory is cheaper and is used instead.
 //
 // Random draws: element i uses logical lane j = i mod k and counter i div k;
-// for power-of-two k <= 256 the k lane bases are staged in shared memory.
-// The selected target travels with the candidate (no dependent reload).
+// for power-of-two k <= 256 each lane stages the words of its own 4 slots
+// (stage_words), and an accept prefilter skips the full draw for elements
+// that cannot be accepted (dprs_n2v_pow2).
 // ---------------------------------------------------------------------------
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
@@ -955,8 +956,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
 
 // Node2Vec DPRS, exact order, prev >= 0, any k (lane bases recomputed per
 // element; the correctness path for non-power-of-two lane widths).
-template <int KMODE>
-__device__ uint32_t dprs_n2v_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
+__device__ uint32_t dprs_n2v_generic(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                    uint32_t woff, uint32_t &sel_u) {
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
@@ -1151,7 +1151,7 @@ walk_kernel(const WalkArgs a) {
                             sel = a.fac32 ? dprs_n2v_pow2<true>(a, s, k, lane, woff, sel_u)
                                           : dprs_n2v_pow2<false>(a, s, k, lane, woff, sel_u);
                         } else {
-                            sel = dprs_n2v_exact<0>(a, s, k, lane, woff, sel_u);
+                            sel = dprs_n2v_generic(a, s, k, lane, woff, sel_u);
                             have_u = true;
                         }
                     } else {

@@ -54,7 +54,7 @@ struct WalkArgs {
     double fac[4];  // node2vec factor by 2*is_prev + is_member: {1/b, 1, 1/a, 1/a}
     int64_t k_small, k_big, d_t;
     uint64_t h;  // mix64(seed + GOLDEN), hoisted stream-key hash
-    uint32_t merge_ratio;  // node2vec: hash N(prev) when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
+    uint32_t merge_ratio;  // node2vec: N(prev) windows when d_prev <= ratio*d_cur + 2*kChunk, else bsearch
     float accept_wmax;     // upper bound on any app weight (exact node2vec accept prefilter)
     // node2vec: 1/a and 1/b are powers of two and w * {1/a, 1/b} is exact in
     // fp32 for every weight, so factor * weight is formed in fp32 and widened

@@ -353,3 +353,46 @@ def test_overlapped_d2h_pieces_bit_exact(s16):
                                app="node2vec", length=40, a=2.0, b=0.5, seed=5)
     np.testing.assert_array_equal(ln, oln)
     np.testing.assert_array_equal(seq.reshape(len(starts), -1), oseq)
+
+
+def _clustered_multigraph(seed=11):
+    """Hubs whose neighbour lists are long contiguous id ranges with repeated
+    entries (multi-edges), overlapping between hubs, plus random edges: skewed
+    bucket maps, duplicate keys across 256-slot window boundaries, full
+    groups (continuation probes), window advances and the bsearch path."""
+    rs = np.random.default_rng(seed)
+    V = 8000
+    src, dst = [], []
+    for h in range(12):
+        lo = 400 * h + 20
+        nb = np.arange(lo, lo + 2500 + 300 * (h % 4))
+        rep = rs.integers(1, 4, len(nb))          # 1-3 copies of each neighbour
+        nb = np.repeat(nb, rep)
+        src.append(np.full(len(nb), h)); dst.append(nb)
+    m = 30000
+    src.append(rs.integers(0, V, m)); dst.append(rs.integers(0, V, m))
+    s = np.concatenate(src); d = np.concatenate(dst)
+    s, d = np.concatenate([s, d]), np.concatenate([d, s])   # symmetrize
+    order = np.lexsort((d, s))
+    s, d = s[order], d[order]
+    off = np.zeros(V + 1, np.int64)
+    np.add.at(off, s + 1, 1)
+    off = np.cumsum(off)
+    w = rs.uniform(1.0, 5.0, len(d)).astype(np.float32)
+    return fw.Graph(V, len(d), off, d.astype(np.uint32), w, None)
+
+
+@pytest.mark.parametrize("eng", [dict(), dict(k_small=4, k_big=8, degree_threshold=6),
+                                 dict(k_small=32, k_big=256, degree_threshold=64)])
+def test_node2vec_clustered_multigraph_matches_oracle(eng):
+    g = _clustered_multigraph()
+    starts = np.concatenate([np.arange(g.vertex_count, dtype=np.int64),
+                             np.repeat(np.arange(12, dtype=np.int64), 200)])
+    app = dict(app="node2vec", length=24, a=2.0, b=0.5)
+    seq, ln, st = _run(g, starts, fw.AppConfig(**app), fw.EngineConfig(replay=True, **eng), 4)
+    kw = dict(app)
+    kw.update({k: v for k, v in eng.items()})
+    oseq, oln, ost = oracle.walk(g.offsets, g.targets, g.weights, None, starts, seed=4, **kw)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq, oseq)
+    assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()

@@ -770,7 +770,7 @@ __device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s,
 // per-lane table, and the accept test.
 template <bool F32>
 __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
-                                  uint32_t woff, uint32_t &sel_u) {
+                                  uint32_t woff) {
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
     const uint32_t off = (uint32_t)(s.elo & 3);
@@ -1148,8 +1148,8 @@ walk_kernel(const WalkArgs a) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
-                            sel = a.fac32 ? dprs_n2v_pow2<true>(a, s, k, lane, woff, sel_u)
-                                          : dprs_n2v_pow2<false>(a, s, k, lane, woff, sel_u);
+                            sel = a.fac32 ? dprs_n2v_pow2<true>(a, s, k, lane, woff)
+                                          : dprs_n2v_pow2<false>(a, s, k, lane, woff);
                         } else {
                             sel = dprs_n2v_generic(a, s, k, lane, woff, sel_u);
                             have_u = true;

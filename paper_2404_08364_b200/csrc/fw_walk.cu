@@ -1196,7 +1196,7 @@ walk_kernel(const WalkArgs a) {
         }
         if (lane == 0) a.out_len[qi] = emitted;
         if (a.done) {  // publish the finished row for the overlapped D2H
-            __threadfence_system();
+            __threadfence();  // gpu scope: the copy engine reads through L2
             __syncwarp();
             if (lane == 0) atomicAdd(a.done + qi / a.piece_q, 1u);
         }

@@ -61,7 +61,7 @@ struct WalkArgs {
     int32_t fac32;
     float inv_a32, inv_b32;
     // per-piece completion counters (null: off).  A warp that finishes
-    // query qi bumps done[qi / piece_q] after a system-scope fence, so the
+    // query qi bumps done[qi / piece_q] after a device-scope fence, so the
     // host's copy stream can wait on a piece (cuStreamWaitValue32) and copy
     // its paths back while the walk continues.
     unsigned *done;

@@ -81,6 +81,10 @@ struct fw_graph {
     DevBuf starts, seq, len, stats, schema, done;
     std::vector<DevBuf> schema_ring;
     int sm_count = 0;
+    // fw_walk's streams and events, created on first use and kept (creating
+    // them per call cost tens of microseconds against millisecond walks)
+    cudaStream_t walk_st = nullptr, copy_st = nullptr;
+    cudaEvent_t ev[6] = {};
 };
 
 extern "C" const char *fw_last_error(void) { return g_err.c_str(); }
@@ -283,6 +287,11 @@ extern "C" int fw_graph_destroy(fw_graph *g) {
     g->stats.release();
     g->schema.release();
     g->done.release();
+    if (g->walk_st) {
+        for (cudaEvent_t e : g->ev) cudaEventDestroy(e);
+        cudaStreamDestroy(g->walk_st);
+        cudaStreamDestroy(g->copy_st);
+    }
     for (auto &b : g->schema_ring) b.release();
     delete g;
     return FW_OK;
@@ -498,15 +507,15 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     const uint64_t P = wv ? kD2hPieces : 0;
     const uint64_t piece_q = P ? (n + P - 1) / P : 0;
     if (P) CU(g->done.reserve(P * sizeof(unsigned)));
-    cudaStream_t st, cs;
-    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    cudaEvent_t e0, e1, e2, e3, ez;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventCreate(&e2);
-    cudaEventCreate(&e3);
-    cudaEventCreateWithFlags(&ez, cudaEventDisableTiming);
+    if (!g->walk_st) {
+        CU(cudaStreamCreateWithFlags(&g->walk_st, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&g->copy_st, cudaStreamNonBlocking));
+        for (int i = 0; i < 4; i++) CU(cudaEventCreate(&g->ev[i]));
+        CU(cudaEventCreateWithFlags(&g->ev[4], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&g->ev[5], cudaEventDisableTiming));
+    }
+    cudaStream_t st = g->walk_st, cs = g->copy_st;
+    cudaEvent_t e0 = g->ev[0], e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3], ez = g->ev[4];
     cudaEventRecord(e0, st);
     cudaMemsetAsync(g->stats.p, 0, ST_WORDS * sizeof(int64_t), st);
     if (P) cudaMemsetAsync(g->done.p, 0, P * sizeof(unsigned), st);
@@ -544,11 +553,8 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         }
         cudaMemcpyAsync(hst, g->stats.p, sizeof(hst), cudaMemcpyDeviceToHost, st);
         if (P) {  // the end event covers both streams
-            cudaEvent_t ec;
-            cudaEventCreateWithFlags(&ec, cudaEventDisableTiming);
-            cudaEventRecord(ec, cs);
-            cudaStreamWaitEvent(st, ec, 0);
-            cudaEventDestroy(ec);
+            cudaEventRecord(g->ev[5], cs);
+            cudaStreamWaitEvent(st, g->ev[5], 0);
         }
         cudaEventRecord(e3, st);
         cudaError_t ce = cudaStreamSynchronize(st);
@@ -577,13 +583,6 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         const uint64_t last = (uint64_t)hst[ST_T_LAST], first = ~(uint64_t)hst[ST_T_FIRST_NEG];
         stats->tail_ms = (n && last >= first) ? (double)(last - first) * 1e-6 : 0.0;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
-    cudaEventDestroy(e3);
-    cudaEventDestroy(ez);
-    cudaStreamDestroy(st);
-    cudaStreamDestroy(cs);
     return rc;
 }
 

@@ -768,7 +768,7 @@ __device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s,
 // ahead) and weights, branch-free membership lookups into the N(prev) table,
 // a 4-element local prefix plus one warp scan, draw words from the staged
 // per-lane table, and the accept test.
-template <bool F32>
+template <bool F32, bool WEIGHTED>
 __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                   uint32_t woff) {
     const uint32_t deg = s.deg;
@@ -811,7 +811,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         float wf[4] = {1.f, 1.f, 1.f, 1.f};
         uint32_t valid = 0xF;
         if (edge) {
-            if (x0 + 4 * lane < span && a.weighted) {
+            if (WEIGHTED && x0 + 4 * lane < span) {
                 const float4 w4 = ldg(reinterpret_cast<const float4 *>(
                     reinterpret_cast<const char *>(tp) + wdelta));
                 wf[0] = w4.x; wf[1] = w4.y; wf[2] = w4.z; wf[3] = w4.w;
@@ -823,7 +823,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                     wf[e] = 0.0f;
                 }
             }
-        } else if (a.weighted) {
+        } else if (WEIGHTED) {
             const float4 w4 = ldg(reinterpret_cast<const float4 *>(
                 reinterpret_cast<const char *>(tp) + wdelta));
             wf[0] = w4.x; wf[1] = w4.y; wf[2] = w4.z; wf[3] = w4.w;
@@ -1148,8 +1148,12 @@ walk_kernel(const WalkArgs a) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
-                            sel = a.fac32 ? dprs_n2v_pow2<true>(a, s, k, lane, woff)
-                                          : dprs_n2v_pow2<false>(a, s, k, lane, woff);
+                            if (a.weighted)
+                                sel = a.fac32 ? dprs_n2v_pow2<true, true>(a, s, k, lane, woff)
+                                              : dprs_n2v_pow2<false, true>(a, s, k, lane, woff);
+                            else
+                                sel = a.fac32 ? dprs_n2v_pow2<true, false>(a, s, k, lane, woff)
+                                              : dprs_n2v_pow2<false, false>(a, s, k, lane, woff);
                         } else {
                             sel = dprs_n2v_generic(a, s, k, lane, woff, sel_u);
                             have_u = true;

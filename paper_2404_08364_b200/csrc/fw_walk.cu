@@ -768,14 +768,15 @@ __device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s,
 // ahead) and weights, branch-free membership lookups into the N(prev) table,
 // a 4-element local prefix plus one warp scan, draw words from the staged
 // per-lane table, and the accept test.
-template <bool F32, bool WEIGHTED>
+// HASHED: the caller has established that N(prev) uses windows (not bsearch).
+template <bool F32, bool WEIGHTED, bool HASHED = false>
 __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                   uint32_t woff) {
     const uint32_t deg = s.deg;
     const uint32_t prev = (uint32_t)s.prev;
     const uint32_t off = (uint32_t)(s.elo & 3);
     const uint32_t dp = (uint32_t)(s.phi - s.plo);
-    const bool use_hash = dp <= a.merge_ratio * deg + 2 * kChunk;
+    const bool use_hash = HASHED || dp <= a.merge_ratio * deg + 2 * kChunk;
     const uint32_t span = deg + off;
     // this lane's 4-slot group of tile 0 (16-byte aligned: the tile grid is
     // anchored at elo & ~3); weights sit at a fixed byte distance
@@ -1149,7 +1150,10 @@ walk_kernel(const WalkArgs a) {
                     if (s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
                             if (a.weighted)
-                                sel = a.fac32 ? dprs_n2v_pow2<true, true>(a, s, k, lane, woff)
+                                sel = a.fac32 ? ((uint32_t)(s.phi - s.plo) <=
+                                                         a.merge_ratio * s.deg + 2 * kChunk
+                                                     ? dprs_n2v_pow2<true, true, true>(a, s, k, lane, woff)
+                                                     : dprs_n2v_pow2<true, true>(a, s, k, lane, woff))
                                               : dprs_n2v_pow2<false, true>(a, s, k, lane, woff);
                             else
                                 sel = a.fac32 ? dprs_n2v_pow2<true, false>(a, s, k, lane, woff)

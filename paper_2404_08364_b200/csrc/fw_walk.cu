@@ -897,6 +897,10 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         const double p1 = __dadd_rn(wv[0], wv[1]);
         const double p2 = __dadd_rn(p1, wv[2]);
         const double p3 = __dadd_rn(p2, wv[3]);
+        // prefilter threshold from the tile's starting carry (<= every
+        // lane's base, so the bound below stays valid); it does not wait
+        // for the scan
+        const uint32_t thr = accept_thr(a.accept_wmax, carry);
         const double incl = warp_incl_scan_p(p3);
         const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
         carry = __dadd_rn(carry, shfl_d(incl, 31));
@@ -911,13 +915,12 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                                 (((uint64_t)qb.w << 32) | qb.z) + cg};
 #if FW_PREFILTER
         // Accept prefilter.  Element e is accepted iff w > 0 and fl(r*P) < w
-        // with P = base + pre[e] >= base + w, which implies r < w/(base + w)
-        // <= wmax/(base + wmax) = T, i.e. hi32(z) <= floor(T*2^32).  hi32(z)
+        // with P = base + pre[e] >= carry + w, which implies r < w/(carry + w)
+        // <= wmax/(carry + wmax) = T, i.e. hi32(z) <= floor(T*2^32).  hi32(z)
         // differs from hi32(y) (y = the second multiply, before the final
         // xorshift) only in bit 0, so the fast path stops after the second
         // multiply's high word and compares it against thr >= floor(T*2^32)+2
         // (base = 0 -> all pass).  Elements that pass run the exact test.
-        const uint32_t thr = accept_thr(a.accept_wmax, base);
         uint32_t pass = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;

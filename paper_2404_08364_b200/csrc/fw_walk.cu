@@ -26,6 +26,10 @@ namespace fw {
 // Cold helpers (window advance, hash build, binary-search fallback).
 // Inlined by default: an out-of-line call makes the tile loop save and
 // restore registers around it (measured 6.3e7 vs 5.4e7 steps/s).
+#ifndef FW_PF_NEXT
+#define FW_PF_NEXT 1
+#endif
+
 #ifndef FW_PREFETCH_CHUNK
 #define FW_PREFETCH_CHUNK 1
 #endif
@@ -935,7 +939,15 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                 run = __dadd_rn(run, w);
                 if ((pass >> e) & 1) {
                     const double r = u01_word(wd[e]);
-                    if (w > 0.0 && __dmul_rn(r, run) < w) cand = (uint32_t)(i0 + e) + 1;
+                    if (w > 0.0 && __dmul_rn(r, run) < w) {
+                        cand = (uint32_t)(i0 + e) + 1;
+#if FW_PF_NEXT
+                        // the candidate may become the next vertex: pull its
+                        // CSR offsets toward this SM now (the target itself
+                        // was loaded by this tile, L1-resident)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.off + __ldg(tp + e)));
+#endif
+                    }
                 }
             }
         }

@@ -511,8 +511,12 @@ __device__ __forceinline__ void tab_clear(uint32_t woff, int lane) {
 }
 
 __device__ __forceinline__ uint32_t tab_scale(uint32_t kmin, uint32_t kmax) {
+    // any scale keeps the bucket map monotone (tab_group clamps the top), so
+    // the approximate reciprocal is enough; range >= 1 is never denormal
     const float range = (float)(kmax - kmin) + 1.0f;
-    return (uint32_t)fminf(__fdividef((float)kGroups * 4294967296.0f, range), 4294967040.0f);
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(range));
+    return (uint32_t)fminf((float)kGroups * 4294967296.0f * r, 4294967040.0f);
 }
 
 // The keys of chunk c, loaded ahead of the build so the load latency can

@@ -309,7 +309,8 @@ extern "C" int fw_graph_info_get(fw_graph *g, fw_graph_info *out) {
 // all fp64 partial sums are exact and any summation order reproduces the
 // reference's sequential `run += w` bit-for-bit.
 // ---------------------------------------------------------------------------
-static bool exact_order_ok(const fw_graph_info &gi, const fw_app &app) {
+static bool exact_order_ok(const fw_graph_info &gi, const fw_app &app, long *g_out = nullptr,
+                           double *xmax_out = nullptr) {
     if (gi.reserved) return false;  // non-finite or negative weights: be literal
     std::vector<double> F{1.0};
     if (app.app_id == FW_APP_NODE2VEC) {
@@ -339,6 +340,8 @@ static bool exact_order_ok(const fw_graph_info &gi, const fw_app &app) {
         }
     }
     if (G < -1000) return false;
+    if (g_out) *g_out = G;
+    if (xmax_out) *xmax_out = xmax;
     const double lim = std::ldexp(1.0, (int)(52 + G));
     return (double)gi.max_degree * xmax <= lim;
 }
@@ -366,7 +369,9 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
                   int *grid_out, unsigned *d_done = nullptr, uint64_t piece_q = 0) {
     if (base_qid + n > (1ull << 33))
         return set_err(FW_ECONFIG, "query ids exceed the replay stream-id field (2^33)");
-    const bool exact = eng->order_mode == FW_ORDER_AUTO && exact_order_ok(g->info, *app);
+    long G = 0;
+    double xmax = 0.0;
+    const bool exact = eng->order_mode == FW_ORDER_AUTO && exact_order_ok(g->info, *app, &G, &xmax);
     if (exact_out) *exact_out = exact;
     if (n == 0) return FW_OK;
     WalkArgs a{};
@@ -417,6 +422,18 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         a.fac32 = ok && !(env && env[0] == '0') ? 1 : 0;
         a.inv_a32 = (float)app->inv_a;
         a.inv_b32 = (float)app->inv_b;
+    }
+    {   // integer tile sums (node2vec fp32 factor path): every app weight is
+        // an integer multiple of 2^G, so w * 2^-G is an exact integer; a
+        // lane's 4 of them must fit a u32 and the scaled prefilter bound
+        // must stay finite
+        const double sc = std::ldexp(1.0, (int)-G);
+        const char *env = getenv("FW_ISCAN");  // A/B override: 0 forces the fp64 tile scan
+        a.iscan = exact && a.fac32 && G >= -126 && G <= 126 && 4.0 * xmax * sc < 2147483648.0 &&
+                  !(env && env[0] == '0') ? 1 : 0;
+        a.iscale = a.iscan ? (float)sc : 1.0f;
+        const double ws = (double)a.accept_wmax * sc;
+        a.accept_wmax_s = a.iscan && std::isfinite(ws) && ws <= 1e37 ? (float)ws : INFINITY;
     }
     a.k_small = eng->k_small;
     a.k_big = eng->k_big;

@@ -719,13 +719,15 @@ __device__ __forceinline__ uint32_t mix64_yhi(uint64_t z) {
 // estimate of T (conversion, add, approximate reciprocal, multiply) is within
 // 2^-20 relative; the 2^-12 margin covers it.  base beyond the fp32 range gives
 // t = 0 and thr = 2, still >= floor(T * 2^32) + 2 = 2.
-__device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
-    const float b = (float)base;
+__device__ __forceinline__ uint32_t accept_thr_f(float wmax, float b) {
     float r;  // MUFU.RCP without the denormal-range fixup of __fdividef
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b + wmax));
     const float t = wmax * r;
     const uint32_t thr = __float2uint_rz(fmaf(t, 4294967296.0f * 1.000244140625f, 2.0f));
     return wmax <= 1e37f ? thr : 0xFFFFFFFFu;  // the host passes +inf to disable
+}
+__device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
+    return accept_thr_f(wmax, (float)base);
 }
 
 // 64-bit warp shuffle from an arbitrary source lane.
@@ -777,7 +779,7 @@ __device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s,
 // a 4-element local prefix plus one warp scan, draw words from the staged
 // per-lane table, and the accept test.
 // HASHED: the caller has established that N(prev) uses windows (not bsearch).
-template <bool F32, bool WEIGHTED, bool HASHED = false>
+template <bool F32, bool WEIGHTED, bool HASHED = false, bool ISCAN = false>
 __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                   uint32_t woff) {
     const uint32_t deg = s.deg;
@@ -808,6 +810,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     const uint32_t cmul = k == 256 ? 0 : (128u >> (31 - __clz(k)));
     const uint32_t wq0 = (woff + kTabSlots) * 4 + 16 * lane;  // staged words (bytes)
     double carry = 0.0;
+    uint64_t icarry = 0;  // ISCAN: the carry in units of 2^G (exact)
     uint32_t cand = 0;
     const uint32_t ntiles = (span + 127) >> 7;
     for (uint32_t t = 0; t < ntiles; t++, tp += 128) {
@@ -892,6 +895,53 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                     wp[e] = (u[e] == prev ? a.inv_a32 : (((mem >> e) & 1) ? 1.0f : a.inv_b32)) * wf[e];
             }
         }
+        // draw words: staged per-lane words + counter(t) * GOLDEN
+        const uint32_t wq = wq0 + (cmul ? 0 : (t & 1) * 1024);
+        if constexpr (ISCAN) {
+            // Integer tile sums.  Every app weight is an integer multiple of
+            // 2^G, so wi = w * 2^-G is exact (FMUL by a power of two, F2I)
+            // and the tile total is two 16-bit-half warp reductions
+            // (REDUX); the carry stays an exact u64.  The fp64 prefix scan
+            // runs only in tiles where some element passes the prefilter
+            // (a scale by a power of two commutes with fp64 rounding, so
+            // fl(r * P') < w' in units of 2^G is the reference's test).
+            uint32_t wi[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) wi[e] = __float2uint_rz(wp[e] * a.iscale);
+            const uint32_t li = (wi[0] + wi[1]) + (wi[2] + wi[3]);
+            const uint32_t thr = accept_thr_f(a.accept_wmax_s, (float)icarry);
+            const uint32_t slo = __reduce_add_sync(FULL, li & 0xFFFFu);
+            const uint32_t shi = __reduce_add_sync(FULL, li >> 16);
+            const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
+            const uint4 qb = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq + 512);
+            const uint64_t cg = (uint64_t)(cmul ? t * cmul : t >> 1) * GOLDEN;
+            const uint64_t wd[4] = {(((uint64_t)qa.y << 32) | qa.x) + cg,
+                                    (((uint64_t)qa.w << 32) | qa.z) + cg,
+                                    (((uint64_t)qb.y << 32) | qb.x) + cg,
+                                    (((uint64_t)qb.w << 32) | qb.z) + cg};
+            uint32_t pass = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;
+            pass &= valid;
+            if (__any_sync(FULL, pass)) {
+                const double l3 = (double)li;
+                const double incl = warp_incl_scan_p(l3);
+                double run = __dadd_rn((double)icarry, __dadd_rn(incl, -l3));  // exact
+                if (pass) {
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const double w = (double)wi[e];
+                        run = __dadd_rn(run, w);
+                        if ((pass >> e) & 1) {
+                            const double r = u01_word(wd[e]);
+                            if (w > 0.0 && __dmul_rn(r, run) < w) cand = (uint32_t)(i0 + e) + 1;
+                        }
+                    }
+                }
+            }
+            icarry += ((uint64_t)shi << 16) + slo;
+            continue;
+        }
         double wv[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
@@ -912,8 +962,6 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         const double incl = warp_incl_scan_p(p3);
         const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
         carry = __dadd_rn(carry, shfl_d(incl, 31));
-        // draw words: staged per-lane words + counter(t) * GOLDEN
-        const uint32_t wq = wq0 + (cmul ? 0 : (t & 1) * 1024);
         const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
         const uint4 qb = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq + 512);
         const uint64_t cg = (uint64_t)(cmul ? t * cmul : t >> 1) * GOLDEN;
@@ -1168,15 +1216,18 @@ walk_kernel(const WalkArgs a) {
                 if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
+                            const bool win = (uint32_t)(s.phi - s.plo) <=
+                                             a.merge_ratio * s.deg + 2 * kChunk;
                             if (a.weighted)
-                                sel = a.fac32 ? ((uint32_t)(s.phi - s.plo) <=
-                                                         a.merge_ratio * s.deg + 2 * kChunk
-                                                     ? dprs_n2v_pow2<true, true, true>(a, s, k, lane, woff)
-                                                     : dprs_n2v_pow2<true, true>(a, s, k, lane, woff))
-                                              : dprs_n2v_pow2<false, true>(a, s, k, lane, woff);
+                                sel = a.iscan ? (win ? dprs_n2v_pow2<true, true, true, true>(a, s, k, lane, woff)
+                                                     : dprs_n2v_pow2<true, true, false, true>(a, s, k, lane, woff))
+                                      : a.fac32 ? (win ? dprs_n2v_pow2<true, true, true>(a, s, k, lane, woff)
+                                                       : dprs_n2v_pow2<true, true>(a, s, k, lane, woff))
+                                                : dprs_n2v_pow2<false, true>(a, s, k, lane, woff);
                             else
-                                sel = a.fac32 ? dprs_n2v_pow2<true, false>(a, s, k, lane, woff)
-                                              : dprs_n2v_pow2<false, false>(a, s, k, lane, woff);
+                                sel = a.iscan ? dprs_n2v_pow2<true, false, false, true>(a, s, k, lane, woff)
+                                      : a.fac32 ? dprs_n2v_pow2<true, false>(a, s, k, lane, woff)
+                                                : dprs_n2v_pow2<false, false>(a, s, k, lane, woff);
                         } else {
                             sel = dprs_n2v_generic(a, s, k, lane, woff, sel_u);
                             have_u = true;

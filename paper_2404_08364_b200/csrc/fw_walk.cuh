@@ -60,6 +60,10 @@ struct WalkArgs {
     // fp32 for every weight, so factor * weight is formed in fp32 and widened
     int32_t fac32;
     float inv_a32, inv_b32;
+    // node2vec fp32 factor path in exact order: tile sums as integers in
+    // units of 2^G (iscale = 2^-G); accept_wmax_s = accept_wmax * 2^-G
+    int32_t iscan;
+    float iscale, accept_wmax_s;
     // per-piece completion counters (null: off).  A warp that finishes
     // query qi bumps done[qi / piece_q] after a device-scope fence, so the
     // host's copy stream can wait on a piece (cuStreamWaitValue32) and copy

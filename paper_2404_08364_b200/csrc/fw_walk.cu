@@ -856,7 +856,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                 const uint4 q = bucket_at(woff, tab_group(u[e], hs));
                 const bool hit = bucket_has(q, u[e]);
                 if constexpr (F32) {
-                    wp[e] = (u[e] == prev ? a.inv_a32 : (hit ? 1.0f : a.inv_b32)) * wf[e];
+                    wp[e] = (u[e] == prev ? a.fa32 : (hit ? a.f132 : a.fb32)) * wf[e];
                 } else {
                     mem |= (hit ? 1u : 0u) << e;
                 }
@@ -882,7 +882,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                 if constexpr (F32) {
 #pragma unroll
                     for (int e = 0; e < 4; e++)
-                        if (((sr.mem >> e) & 1) && u[e] != prev) wp[e] = wf[e];
+                        if (((sr.mem >> e) & 1) && u[e] != prev) wp[e] = a.f132 * wf[e];
                 } else {
                     mem |= sr.mem;
                 }
@@ -892,14 +892,15 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             if constexpr (F32) {
 #pragma unroll
                 for (int e = 0; e < 4; e++)
-                    wp[e] = (u[e] == prev ? a.inv_a32 : (((mem >> e) & 1) ? 1.0f : a.inv_b32)) * wf[e];
+                    wp[e] = (u[e] == prev ? a.fa32 : (((mem >> e) & 1) ? a.f132 : a.fb32)) * wf[e];
             }
         }
         // draw words: staged per-lane words + counter(t) * GOLDEN
         const uint32_t wq = wq0 + (cmul ? 0 : (t & 1) * 1024);
         if constexpr (ISCAN) {
             // Integer tile sums.  Every app weight is an integer multiple of
-            // 2^G, so wi = w * 2^-G is exact (FMUL by a power of two, F2I)
+            // 2^G, so wi = w * 2^-G is exact (the factors fa32/f132/fb32
+            // carry the 2^-G, then F2I)
             // and the tile total is two 16-bit-half warp reductions
             // (REDUX); the carry stays an exact u64.  The fp64 prefix scan
             // runs only in tiles where some element passes the prefilter
@@ -907,7 +908,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             // fl(r * P') < w' in units of 2^G is the reference's test).
             uint32_t wi[4];
 #pragma unroll
-            for (int e = 0; e < 4; e++) wi[e] = __float2uint_rz(wp[e] * a.iscale);
+            for (int e = 0; e < 4; e++) wi[e] = __float2uint_rz(wp[e]);  // factors carry 2^-G
             const uint32_t li = (wi[0] + wi[1]) + (wi[2] + wi[3]);
             const uint32_t thr = accept_thr_f(a.accept_wmax_s, (float)icarry);
             const uint32_t slo = __reduce_add_sync(FULL, li & 0xFFFFu);
@@ -940,80 +941,80 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                 }
             }
             icarry += ((uint64_t)shi << 16) + slo;
-            continue;
-        }
-        double wv[4];
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            if constexpr (F32) {
-                wv[e] = (double)wp[e];
-            } else {
-                const double f = u[e] == prev ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
-                wv[e] = __dmul_rn(f, (double)wf[e]);
-            }
-        }
-        const double p1 = __dadd_rn(wv[0], wv[1]);
-        const double p2 = __dadd_rn(p1, wv[2]);
-        const double p3 = __dadd_rn(p2, wv[3]);
-        // prefilter threshold from the tile's starting carry (<= every
-        // lane's base, so the bound below stays valid); it does not wait
-        // for the scan
-        const uint32_t thr = accept_thr(a.accept_wmax, carry);
-        const double incl = warp_incl_scan_p(p3);
-        const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
-        carry = __dadd_rn(carry, shfl_d(incl, 31));
-        const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
-        const uint4 qb = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq + 512);
-        const uint64_t cg = (uint64_t)(cmul ? t * cmul : t >> 1) * GOLDEN;
-        const uint64_t wd[4] = {(((uint64_t)qa.y << 32) | qa.x) + cg,
-                                (((uint64_t)qa.w << 32) | qa.z) + cg,
-                                (((uint64_t)qb.y << 32) | qb.x) + cg,
-                                (((uint64_t)qb.w << 32) | qb.z) + cg};
-#if FW_PREFILTER
-        // Accept prefilter.  Element e is accepted iff w > 0 and fl(r*P) < w
-        // with P = base + pre[e] >= carry + w, which implies r < w/(carry + w)
-        // <= wmax/(carry + wmax) = T, i.e. hi32(z) <= floor(T*2^32).  hi32(z)
-        // differs from hi32(y) (y = the second multiply, before the final
-        // xorshift) only in bit 0, so the fast path stops after the second
-        // multiply's high word and compares it against thr >= floor(T*2^32)+2
-        // (base = 0 -> all pass).  Elements that pass run the exact test.
-        uint32_t pass = 0;
-#pragma unroll
-        for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;
-        if (pass & valid) {
-            // P = base + w_0 + ... + w_e, recomputed here (every partial sum
-            // is exact, so the association order does not matter) so that
-            // only the fp32 products stay live across the draws
-            double run = base;
+        } else {
+            double wv[4];
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                const double w = F32 ? (double)wp[e] : wv[e];
-                run = __dadd_rn(run, w);
-                if ((pass >> e) & 1) {
-                    const double r = u01_word(wd[e]);
-                    if (w > 0.0 && __dmul_rn(r, run) < w) {
-                        cand = (uint32_t)(i0 + e) + 1;
+                if constexpr (F32) {
+                    wv[e] = (double)wp[e];
+                } else {
+                    const double f = u[e] == prev ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
+                    wv[e] = __dmul_rn(f, (double)wf[e]);
+                }
+            }
+            const double p1 = __dadd_rn(wv[0], wv[1]);
+            const double p2 = __dadd_rn(p1, wv[2]);
+            const double p3 = __dadd_rn(p2, wv[3]);
+            // prefilter threshold from the tile's starting carry (<= every
+            // lane's base, so the bound below stays valid); it does not wait
+            // for the scan
+            const uint32_t thr = accept_thr(a.accept_wmax, carry);
+            const double incl = warp_incl_scan_p(p3);
+            const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
+            carry = __dadd_rn(carry, shfl_d(incl, 31));
+            const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
+            const uint4 qb = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq + 512);
+            const uint64_t cg = (uint64_t)(cmul ? t * cmul : t >> 1) * GOLDEN;
+            const uint64_t wd[4] = {(((uint64_t)qa.y << 32) | qa.x) + cg,
+                                    (((uint64_t)qa.w << 32) | qa.z) + cg,
+                                    (((uint64_t)qb.y << 32) | qb.x) + cg,
+                                    (((uint64_t)qb.w << 32) | qb.z) + cg};
+#if FW_PREFILTER
+            // Accept prefilter.  Element e is accepted iff w > 0 and fl(r*P) < w
+            // with P = base + pre[e] >= carry + w, which implies r < w/(carry + w)
+            // <= wmax/(carry + wmax) = T, i.e. hi32(z) <= floor(T*2^32).  hi32(z)
+            // differs from hi32(y) (y = the second multiply, before the final
+            // xorshift) only in bit 0, so the fast path stops after the second
+            // multiply's high word and compares it against thr >= floor(T*2^32)+2
+            // (base = 0 -> all pass).  Elements that pass run the exact test.
+            uint32_t pass = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;
+            if (pass & valid) {
+                // P = base + w_0 + ... + w_e, recomputed here (every partial sum
+                // is exact, so the association order does not matter) so that
+                // only the fp32 products stay live across the draws
+                double run = base;
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const double w = F32 ? (double)wp[e] : wv[e];
+                    run = __dadd_rn(run, w);
+                    if ((pass >> e) & 1) {
+                        const double r = u01_word(wd[e]);
+                        if (w > 0.0 && __dmul_rn(r, run) < w) {
+                            cand = (uint32_t)(i0 + e) + 1;
 #if FW_PF_NEXT
-                        // the candidate may become the next vertex: pull its
-                        // CSR offsets toward this SM now (the target itself
-                        // was loaded by this tile, L1-resident)
-                        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.off + __ldg(tp + e)));
+                            // the candidate may become the next vertex: pull its
+                            // CSR offsets toward this SM now (the target itself
+                            // was loaded by this tile, L1-resident)
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.off + __ldg(tp + e)));
 #endif
+                        }
                     }
                 }
             }
-        }
 #else
-        const double pre[4] = {wv[0], p1, p2, p3};
+            const double pre[4] = {wv[0], p1, p2, p3};
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const double r = u01_word(wd[e]);
-            const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
-            if (wv[e] > 0.0 && Pr < wv[e]) {
-                cand = (uint32_t)(i0 + e) + 1;
+            for (int e = 0; e < 4; e++) {
+                const double r = u01_word(wd[e]);
+                const double Pr = __dmul_rn(r, __dadd_rn(base, pre[e]));
+                if (wv[e] > 0.0 && Pr < wv[e]) {
+                    cand = (uint32_t)(i0 + e) + 1;
+                }
             }
-        }
 #endif
+        }
     }
     // the selected target is reloaded by the caller (L1/L2-resident): not
     // carrying it frees the u registers before the draws

@@ -62,8 +62,10 @@ struct WalkArgs {
     float inv_a32, inv_b32;
     // node2vec fp32 factor path in exact order: tile sums as integers in
     // units of 2^G (iscale = 2^-G); accept_wmax_s = accept_wmax * 2^-G
+    // fa32/f132/fb32 = {1/a, 1, 1/b} (* 2^-G when iscan): the fp32 factors
     int32_t iscan;
     float iscale, accept_wmax_s;
+    float fa32, f132, fb32;
     // per-piece completion counters (null: off).  A warp that finishes
     // query qi bumps done[qi / piece_q] after a device-scope fence, so the
     // host's copy stream can wait on a piece (cuStreamWaitValue32) and copy

@@ -429,12 +429,12 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         // must stay finite
         const double sc = std::ldexp(1.0, (int)-G);
         const char *env = getenv("FW_ISCAN");  // A/B override: 0 forces the fp64 tile scan
+        const double ws = (double)a.accept_wmax * sc;  // the kernel's prefilter has no disable
         a.iscan = exact && a.fac32 && G >= -126 && G <= 126 && 4.0 * xmax * sc < 2147483648.0 &&
-                  std::max({1.0, app->inv_a, app->inv_b}) * sc <= 1e37 &&
-                  !(env && env[0] == '0') ? 1 : 0;
+                  std::max({1.0, app->inv_a, app->inv_b}) * sc <= 1e37 && std::isfinite(ws) &&
+                  ws <= 1e37 && !(env && env[0] == '0') ? 1 : 0;
         a.iscale = a.iscan ? (float)sc : 1.0f;
-        const double ws = (double)a.accept_wmax * sc;
-        a.accept_wmax_s = a.iscan && std::isfinite(ws) && ws <= 1e37 ? (float)ws : INFINITY;
+        a.accept_wmax_s = a.iscan ? (float)ws : INFINITY;
         a.fa32 = a.inv_a32 * a.iscale;  // powers of two: exact
         a.f132 = a.iscale;
         a.fb32 = a.inv_b32 * a.iscale;

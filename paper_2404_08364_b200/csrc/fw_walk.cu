@@ -719,11 +719,15 @@ __device__ __forceinline__ uint32_t mix64_yhi(uint64_t z) {
 // estimate of T (conversion, add, approximate reciprocal, multiply) is within
 // 2^-20 relative; the 2^-12 margin covers it.  base beyond the fp32 range gives
 // t = 0 and thr = 2, still >= floor(T * 2^32) + 2 = 2.
-__device__ __forceinline__ uint32_t accept_thr_f(float wmax, float b) {
+// Without the disable check (finite wmax <= 1e37 guaranteed by the host).
+__device__ __forceinline__ uint32_t accept_thr_raw(float wmax, float b) {
     float r;  // MUFU.RCP without the denormal-range fixup of __fdividef
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b + wmax));
     const float t = wmax * r;
-    const uint32_t thr = __float2uint_rz(fmaf(t, 4294967296.0f * 1.000244140625f, 2.0f));
+    return __float2uint_rz(fmaf(t, 4294967296.0f * 1.000244140625f, 2.0f));  // saturating
+}
+__device__ __forceinline__ uint32_t accept_thr_f(float wmax, float b) {
+    const uint32_t thr = accept_thr_raw(wmax, b);
     return wmax <= 1e37f ? thr : 0xFFFFFFFFu;  // the host passes +inf to disable
 }
 __device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
@@ -910,7 +914,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
 #pragma unroll
             for (int e = 0; e < 4; e++) wi[e] = __float2uint_rz(wp[e]);  // factors carry 2^-G
             const uint32_t li = (wi[0] + wi[1]) + (wi[2] + wi[3]);
-            const uint32_t thr = accept_thr_f(a.accept_wmax_s, (float)icarry);
+            const uint32_t thr = accept_thr_raw(a.accept_wmax_s, (float)icarry);
             const uint32_t slo = __reduce_add_sync(FULL, li & 0xFFFFu);
             const uint32_t shi = __reduce_add_sync(FULL, li >> 16);
             const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
@@ -920,20 +924,21 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                                     (((uint64_t)qa.w << 32) | qa.z) + cg,
                                     (((uint64_t)qb.y << 32) | qb.x) + cg,
                                     (((uint64_t)qb.w << 32) | qb.z) + cg};
-            uint32_t pass = 0;
+            // invalid slots (wi = 0) may pass; the w > 0 test rejects them
+            uint32_t y[4];
 #pragma unroll
-            for (int e = 0; e < 4; e++) pass |= (mix64_yhi(wd[e]) <= thr ? 1u : 0u) << e;
-            pass &= valid;
-            if (__any_sync(FULL, pass)) {
+            for (int e = 0; e < 4; e++) y[e] = mix64_yhi(wd[e]);
+            const uint32_t ymin = min(min(y[0], y[1]), min(y[2], y[3]));
+            if (__any_sync(FULL, ymin <= thr)) {
                 const double l3 = (double)li;
                 const double incl = warp_incl_scan_p(l3);
                 double run = __dadd_rn((double)icarry, __dadd_rn(incl, -l3));  // exact
-                if (pass) {
+                if (ymin <= thr) {
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
                         const double w = (double)wi[e];
                         run = __dadd_rn(run, w);
-                        if ((pass >> e) & 1) {
+                        if (y[e] <= thr) {
                             const double r = u01_word(wd[e]);
                             if (w > 0.0 && __dmul_rn(r, run) < w) cand = (uint32_t)(i0 + e) + 1;
                         }

@@ -793,9 +793,9 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     const bool use_hash = HASHED || dp <= a.merge_ratio * deg + 2 * kChunk;
     const uint32_t span = deg + off;
     // this lane's 4-slot group of tile 0 (16-byte aligned: the tile grid is
-    // anchored at elo & ~3); weights sit at a fixed byte distance
+    // anchored at elo & ~3); the weights pointer steps alongside
     const uint32_t *tp = a.tgt + (s.elo - off) + 4 * lane;
-    const int64_t wdelta = reinterpret_cast<const char *>(a.w) - reinterpret_cast<const char *>(a.tgt);
+    const float *wpt = a.w + (s.elo - off) + 4 * lane;
     // N(prev)'s start lives in the control words (read by the cold paths)
     if (lane == 0) {
         fw_smem[woff + kCtlWord + 4] = (uint32_t)s.plo;
@@ -817,7 +817,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     uint64_t icarry = 0;  // ISCAN: the carry in units of 2^G (exact)
     uint32_t cand = 0;
     const uint32_t ntiles = (span + 127) >> 7;
-    for (uint32_t t = 0; t < ntiles; t++, tp += 128) {
+    for (uint32_t t = 0; t < ntiles; t++, tp += 128, wpt += 128) {
         const uint32_t x0 = t * 128;  // first slot of the tile
         // interior tile: all 128 slots are elements of N(cur)
         const bool edge = x0 < off || x0 + 128 > span;
@@ -828,8 +828,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
         uint32_t valid = 0xF;
         if (edge) {
             if (WEIGHTED && x0 + 4 * lane < span) {
-                const float4 w4 = ldg(reinterpret_cast<const float4 *>(
-                    reinterpret_cast<const char *>(tp) + wdelta));
+                const float4 w4 = ldg(reinterpret_cast<const float4 *>(wpt));
                 wf[0] = w4.x; wf[1] = w4.y; wf[2] = w4.z; wf[3] = w4.w;
             }
 #pragma unroll
@@ -840,8 +839,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                 }
             }
         } else if (WEIGHTED) {
-            const float4 w4 = ldg(reinterpret_cast<const float4 *>(
-                reinterpret_cast<const char *>(tp) + wdelta));
+            const float4 w4 = ldg(reinterpret_cast<const float4 *>(wpt));
             wf[0] = w4.x; wf[1] = w4.y; wf[2] = w4.z; wf[3] = w4.w;
         }
         if (x0 + 128 < span && x0 + 128 + 4 * lane < span)  // next tile's targets

@@ -396,3 +396,36 @@ def test_node2vec_clustered_multigraph_matches_oracle(eng):
     np.testing.assert_array_equal(ln, oln)
     np.testing.assert_array_equal(seq, oseq)
     assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()
+
+
+def _n2v_weight_sets(n, rs):
+    return {
+        "u15": rs.uniform(1.0, 5.0, n).astype(np.float32),  # integer tile sums, G = -24
+        # small dyadic weights: G = -41, still integer sums (2^41 scale)
+        "dyadic": (rs.integers(1, 1 << 20, n).astype(np.float64) * 2.0 ** -40).astype(np.float32),
+        # 2^-10 .. 2^25: a lane's scaled sum would overflow u32 -> fp64 tile scan
+        "wide": np.where(rs.random(n) < 0.5, 2.0 ** -10, 2.0 ** 25).astype(np.float32),
+        "unweighted": None,
+    }
+
+
+@pytest.mark.parametrize("iscan", ["1", "0"])
+@pytest.mark.parametrize("wset", ["u15", "dyadic", "wide", "unweighted"])
+@pytest.mark.parametrize("ab", [(2.0, 0.5), (0.25, 1.0)])
+def test_node2vec_integer_tile_sums_match_oracle(s16, monkeypatch, iscan, wset, ab):
+    """Node2Vec's integer tile sums (FW_ISCAN, on when every app weight is a
+    multiple of 2^G and a lane's scaled sum fits a u32) and the fp64 tile
+    scan give the oracle's paths for weight sets on both sides of the
+    eligibility test."""
+    monkeypatch.setenv("FW_ISCAN", iscan)
+    rs = np.random.default_rng(17)
+    w = _n2v_weight_sets(s16.edge_count, rs)[wset]
+    g = fw.Graph(s16.vertex_count, s16.edge_count, s16.offsets, s16.targets,
+                 w if w is not None else np.ones(s16.edge_count, np.float32), None)
+    starts = rs.integers(0, g.vertex_count, 12000).astype(np.int64)
+    app = dict(app="node2vec", length=20, a=ab[0], b=ab[1], weighted=w is not None)
+    seq, ln, st = _run(g, starts, fw.AppConfig(**app), fw.EngineConfig(replay=True), 9)
+    oseq, oln, ost = oracle.walk(g.offsets, g.targets, g.weights, None, starts, seed=9, **app)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq, oseq)
+    assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()

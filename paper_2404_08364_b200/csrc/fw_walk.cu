@@ -512,11 +512,19 @@ __device__ __forceinline__ void tab_clear(uint32_t woff, int lane) {
 
 __device__ __forceinline__ uint32_t tab_scale(uint32_t kmin, uint32_t kmax) {
     // any scale keeps the bucket map monotone (tab_group clamps the top), so
-    // the approximate reciprocal is enough; range >= 1 is never denormal
+    // the approximate reciprocal is enough; range >= 1 is never denormal.
+    // The (1 - 2^-18) factor covers the conversion, add, reciprocal and
+    // multiply roundings (< 2^-21 together), so every key of the window maps
+    // below kGroups without the clamp: umulhi(k - kmin, scale) <=
+    // (kmax - kmin) * kGroups / (kmax - kmin + 1) < kGroups (tab_group_in).
     const float range = (float)(kmax - kmin) + 1.0f;
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(range));
-    return (uint32_t)fminf((float)kGroups * 4294967296.0f * r, 4294967040.0f);
+    return (uint32_t)fminf((float)kGroups * 4294967296.0f * (1.0f - 0x1p-18f) * r, 4294967040.0f);
+}
+// Group of a key known to lie in [kmin, kmax] (the build's own keys).
+__device__ __forceinline__ uint32_t tab_group_in(uint32_t k, const HashState &hs) {
+    return __umulhi(k - hs.kmin, hs.scale);
 }
 
 // The keys of chunk c, loaded ahead of the build so the load latency can
@@ -569,7 +577,8 @@ __device__ FW_COLD HashState hash_build(const ChunkKeys &ck, int64_t plo, uint32
     HashState hs;
     int m[8];
     int run = INT_MIN;
-    if (cs >= plo && cs + (int64_t)kChunk <= end) {
+    const bool whole = cs >= plo && cs + (int64_t)kChunk <= end;
+    if (whole) {
         hs.kmin = __shfl_sync(FULL, key[0], 0);
         const uint32_t kmax = __shfl_sync(FULL, key[7], 31);
         hs.scale = tab_scale(hs.kmin, kmax);
@@ -578,7 +587,7 @@ __device__ FW_COLD HashState hash_build(const ChunkKeys &ck, int64_t plo, uint32
         tab_clear(woff, lane);
 #pragma unroll
         for (int r = 0; r < 8; r++) {
-            run = max(run, (int)(4 * tab_group(key[r], hs)) - (s0 + r));
+            run = max(run, (int)(4 * tab_group_in(key[r], hs)) - (s0 + r));
             m[r] = run;
         }
     } else {
@@ -593,7 +602,7 @@ __device__ FW_COLD HashState hash_build(const ChunkKeys &ck, int64_t plo, uint32
         for (int r = 0; r < 8; r++) {
             const int sl = s0 + r;
             const bool v = sl >= vlo && sl < vhi;
-            run = max(run, v ? (int)(4 * tab_group(key[r], hs)) - sl : INT_MIN);
+            run = max(run, v ? (int)(4 * tab_group_in(key[r], hs)) - sl : INT_MIN);
             m[r] = v ? run : INT_MAX;  // INT_MAX marks an invalid slot
         }
     }
@@ -610,10 +619,15 @@ __device__ FW_COLD HashState hash_build(const ChunkKeys &ck, int64_t plo, uint32
     // unconditional stores (no per-key branches): an invalid slot writes
     // kEmpty to the table's last slot, which no key ever occupies (positions
     // stay below 4 (kGroups - 1) + kChunk), so it reads as empty
+    if (whole) {  // every slot valid: no dump redirection
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
-        const bool v = m[r] != INT_MAX;
-        fw_smem[woff + (v ? s0 + r + max(excl, m[r]) : kTabSlots - 1)] = v ? key[r] : kEmpty;
+        for (int r = 0; r < 8; r++) fw_smem[woff + s0 + r + max(excl, m[r])] = key[r];
+    } else {
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const bool v = m[r] != INT_MAX;
+            fw_smem[woff + (v ? s0 + r + max(excl, m[r]) : kTabSlots - 1)] = v ? key[r] : kEmpty;
+        }
     }
     __syncwarp();
     return hs;

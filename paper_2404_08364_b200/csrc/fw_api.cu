@@ -399,7 +399,10 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         const double wm = fmax * (app->weighted ? (double)g->info.max_weight : 1.0);
         float f = (float)wm;
         if ((double)f < wm) f = std::nextafter(f, INFINITY);
-        a.accept_wmax = (std::isfinite(f) && f <= 1e37f) ? f : INFINITY;  // inf: prefilter off
+        // inf: prefilter off.  Negative or non-finite weights (reserved) let
+        // the running prefix shrink, which the prefilter's bound assumes away.
+        const bool lit = app->weighted && g->info.reserved;
+        a.accept_wmax = (std::isfinite(f) && f <= 1e37f && !lit) ? f : INFINITY;
     }
     {   // fp32 factor path: 1/a, 1/b = 2^k and every w * 2^k exact in fp32
         auto pow2_exp = [](double f, int *k) {

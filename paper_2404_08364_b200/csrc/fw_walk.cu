@@ -70,6 +70,34 @@ __device__ __forceinline__ bool in_sorted(const uint32_t *__restrict__ tgt, int6
 }
 
 // Dynamic transition weight of element i of N(cur) (_kernels.py:280-308).
+// High word of the second multiply of mix64 (the final xorshift flips at
+// most bit 0 of it).
+__device__ __forceinline__ uint32_t mix64_yhi(uint64_t z) {
+    z = (z ^ (z >> 30)) * MIX1;
+    z = z ^ (z >> 27);
+    return (uint32_t)((z * MIX2) >> 32);
+}
+
+// Prefilter threshold for a lane whose elements all have prefix P >= base + w:
+// >= floor(T * 2^32) + 2 with T = wmax / (base + wmax), saturated.  The fp32
+// estimate of T (conversion, add, approximate reciprocal, multiply) is within
+// 2^-20 relative; the 2^-12 margin covers it.  base beyond the fp32 range gives
+// t = 0 and thr = 2, still >= floor(T * 2^32) + 2 = 2.
+// Without the disable check (finite wmax <= 1e37 guaranteed by the host).
+__device__ __forceinline__ uint32_t accept_thr_raw(float wmax, float b) {
+    float r;  // MUFU.RCP without the denormal-range fixup of __fdividef
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b + wmax));
+    const float t = wmax * r;
+    return __float2uint_rz(fmaf(t, 4294967296.0f * 1.000244140625f, 2.0f));  // saturating
+}
+__device__ __forceinline__ uint32_t accept_thr_f(float wmax, float b) {
+    const uint32_t thr = accept_thr_raw(wmax, b);
+    return wmax <= 1e37f ? thr : 0xFFFFFFFFu;  // the host passes +inf to disable
+}
+__device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
+    return accept_thr_f(wmax, (float)base);
+}
+
 template <int APP>
 __device__ __forceinline__ double elem_weight(const WalkArgs &a, const StepCtx &s, uint32_t i) {
     const int64_t e = s.elo + i;
@@ -159,25 +187,43 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
     uint32_t cand = 0;
     uint64_t word = lane_base(a, s, j);
     const uint32_t deg = s.deg;
+    // Accept prefilter (as in dprs_n2v_pow2): element accepted => r <
+    // w / (run_before + w) <= wmax / (run_before + wmax), so hi32 of the
+    // draw's second multiply must be <= thr(run at the batch start); only
+    // those elements run the full draw and the exact test.
+    uint32_t i = j;
     if (staged) {
-#pragma unroll 4
-        for (uint32_t i = j; i < deg; i += k, word += GOLDEN) {
+        for (; i + 3 * k < deg; i += 4 * k) {
+            const uint32_t thr = accept_thr(a.accept_wmax, run);
+#pragma unroll
+            for (int r = 0; r < 4; r++, word += GOLDEN) {
+                const double wv = (double)stage[i + r * k];
+                run = __dadd_rn(run, wv);
+                if (mix64_yhi(word) <= thr) {
+                    const double u = u01_word(word);
+                    if (wv > 0.0 && __dmul_rn(u, run) < wv) cand = i + r * k + 1;
+                }
+            }
+        }
+        for (; i < deg; i += k, word += GOLDEN) {
             const double wv = (double)stage[i];
             run = __dadd_rn(run, wv);
             const double r = u01_word(word);
             if (wv > 0.0 && __dmul_rn(r, run) < wv) cand = i + 1;
         }
     } else {
-        uint32_t i = j;
         if constexpr (APP != APP_NODE2VEC) {
             for (; i + 3 * k < deg; i += 4 * k) {
                 double x[4];
                 weights4<APP>(a, s, i, k, x);
+                const uint32_t thr = accept_thr(a.accept_wmax, run);
 #pragma unroll
                 for (int r = 0; r < 4; r++, word += GOLDEN) {
                     run = __dadd_rn(run, x[r]);
-                    const double u = u01_word(word);
-                    if (x[r] > 0.0 && __dmul_rn(u, run) < x[r]) cand = i + r * k + 1;
+                    if (mix64_yhi(word) <= thr) {
+                        const double u = u01_word(word);
+                        if (x[r] > 0.0 && __dmul_rn(u, run) < x[r]) cand = i + r * k + 1;
+                    }
                 }
             }
         }
@@ -718,34 +764,6 @@ __device__ FW_COLD uint32_t member4_bsearch(const uint32_t *__restrict__ P, uint
     for (int e = 0; e < 4; e++)
         if (((need >> e) & 1) && ldg(P + b[e]) == u[e]) mem |= 1u << e;
     return mem;
-}
-
-// High word of the second multiply of mix64 (the final xorshift flips at
-// most bit 0 of it).
-__device__ __forceinline__ uint32_t mix64_yhi(uint64_t z) {
-    z = (z ^ (z >> 30)) * MIX1;
-    z = z ^ (z >> 27);
-    return (uint32_t)((z * MIX2) >> 32);
-}
-
-// Prefilter threshold for a lane whose elements all have prefix P >= base + w:
-// >= floor(T * 2^32) + 2 with T = wmax / (base + wmax), saturated.  The fp32
-// estimate of T (conversion, add, approximate reciprocal, multiply) is within
-// 2^-20 relative; the 2^-12 margin covers it.  base beyond the fp32 range gives
-// t = 0 and thr = 2, still >= floor(T * 2^32) + 2 = 2.
-// Without the disable check (finite wmax <= 1e37 guaranteed by the host).
-__device__ __forceinline__ uint32_t accept_thr_raw(float wmax, float b) {
-    float r;  // MUFU.RCP without the denormal-range fixup of __fdividef
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b + wmax));
-    const float t = wmax * r;
-    return __float2uint_rz(fmaf(t, 4294967296.0f * 1.000244140625f, 2.0f));  // saturating
-}
-__device__ __forceinline__ uint32_t accept_thr_f(float wmax, float b) {
-    const uint32_t thr = accept_thr_raw(wmax, b);
-    return wmax <= 1e37f ? thr : 0xFFFFFFFFu;  // the host passes +inf to disable
-}
-__device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
-    return accept_thr_f(wmax, (float)base);
 }
 
 // 64-bit warp shuffle from an arbitrary source lane.

@@ -52,6 +52,8 @@ def parse_args():
                    choices=["node2vec", "deepwalk", "ppr", "metapath"])
     p.add_argument("--length", type=int, default=None)
     p.add_argument("--queries", default="all", help="all | hub (PPR config)")
+    p.add_argument("--sampler", choices=["auto", "dprs", "zprs"], default="auto",
+                   help="EngineConfig.sampler (auto: DPRS for Node2Vec, else ZPRS)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -180,7 +182,7 @@ def import_reference():
     return E, AppConfig, Graph
 
 
-def reference_runner(host_graph, app, starts_all):
+def reference_runner(host_graph, app, starts_all, sampler="auto"):
     """Returns (kind, run(n, offset) -> (sampled_steps, seconds), cores)."""
     cores = os.cpu_count() or 1
     try:
@@ -189,7 +191,7 @@ def reference_runner(host_graph, app, starts_all):
                     host_graph.targets, host_graph.weights, host_graph.labels)
         rapp = RAppConfig(app=app.app, length=app.length, stop_prob=app.stop_prob, a=app.a,
                           b=app.b, schema=tuple(app.schema), weighted=app.weighted)
-        eng = E.EngineConfig(workers=cores, replay=True)
+        eng = E.EngineConfig(workers=cores, replay=True, sampler=sampler)
 
         def run(n, off):
             total = [0]
@@ -226,8 +228,8 @@ def calibrate(run, seconds):
     return max(64, int(rate_q * seconds))
 
 
-def cpu_baseline(host_graph, app, starts_all, seconds):
-    kind, run, cores = reference_runner(host_graph, app, starts_all)
+def cpu_baseline(host_graph, app, starts_all, seconds, sampler="auto"):
+    kind, run, cores = reference_runner(host_graph, app, starts_all, sampler)
     n = min(calibrate(run, seconds), len(starts_all))
     sampled, t = run(n, 0)
     return {"value": sampled / t, "unit": "steps/s", "cores": cores, "kind": kind,
@@ -250,7 +252,7 @@ def bench_reference(args):
     app = app_config(args)
     g = rmat.rmat_graph(args.scale, labels=(args.app == "metapath"))
     starts = make_starts(args, g.vertex_count, g.max_degree_vertex())
-    kind, run, cores = reference_runner(g, app, starts)
+    kind, run, cores = reference_runner(g, app, starts, args.sampler)
     n = min(calibrate(run, min(args.cpu_seconds, 8.0)), len(starts))
     for i in range(args.warmup):
         run(n, (i * n) % max(1, len(starts) - n))
@@ -265,7 +267,7 @@ def bench_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * tot_t / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp64+u64", "data": "synthetic",
-        "config": {"workload": workload_name(args, app), "graph": f"rmat-s{args.scale}-ef16",
+        "config": {"workload": workload_name(args, app), "graph": f"rmat-s{args.scale}-ef16", "sampler": args.sampler,
                    "sample_queries_per_step": n},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": kind,
                          "sample": f"{n} queries per step, replay mode, workers={cores}"},
@@ -348,7 +350,7 @@ def bench_ours(args):
     seq = torch.empty(n * L, dtype=torch.int32, device=dev)
     lens = torch.empty(n, dtype=torch.int32, device=dev)
     stats = torch.zeros(10, dtype=torch.int64, device=dev)
-    a_s, e_s, _schema = _fw_structs(app, fw.EngineConfig(replay=True))
+    a_s, e_s, _schema = _fw_structs(app, fw.EngineConfig(replay=True, sampler=args.sampler))
     stream = torch.cuda.current_stream(dev)
 
     def launch():
@@ -448,7 +450,7 @@ def bench_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             host = dg.to_host()
-            cpu = cpu_baseline(host, app, starts_h, args.cpu_seconds)
+            cpu = cpu_baseline(host, app, starts_h, args.cpu_seconds, args.sampler)
         except Exception as exc:  # report, never fail the GPU line
             cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {type(exc).__name__}: {exc}"}
@@ -459,7 +461,7 @@ def bench_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "fp64+u64", "data": "synthetic",
-            "config": {"workload": workload, "graph": f"rmat-s{args.scale}-ef16",
+            "config": {"workload": workload, "graph": f"rmat-s{args.scale}-ef16", "sampler": args.sampler,
                        "vertices": V, "csr_entries": E_, "queries_per_gpu": n,
                        "replicate_s": None if world == 1 else round(t_rep, 3),
                        "gather_ms": gather_ms,

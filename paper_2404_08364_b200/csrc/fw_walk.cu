@@ -389,10 +389,13 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
         for (uint32_t t0 = 0; t0 < deg; t0 += 32, word += GOLDEN) {
             const uint32_t i = t0 + lane;
             const double wv = i < deg ? elem_weight<APP>(a, s, i) : 0.0;
+            const uint32_t thr = accept_thr(a.accept_wmax, carry);  // prefilter
             const double incl = warp_incl_scan(wv, lane);
             const double P = __dadd_rn(carry, incl);
-            const double r = u01_word(word);
-            if (wv > 0.0 && __dmul_rn(r, P) < wv) cand = i + 1;
+            if (mix64_yhi(word) <= thr) {
+                const double r = u01_word(word);
+                if (wv > 0.0 && __dmul_rn(r, P) < wv) cand = i + 1;
+            }
             carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
         }
     } else if (k == 256) {
@@ -407,10 +410,14 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
                 if (t0 < deg) {  // warp-uniform
                     const uint32_t i = t0 + lane;
                     const double wv = i < deg ? elem_weight<APP>(a, s, i) : 0.0;
+                    const uint32_t thr = accept_thr(a.accept_wmax, carry);  // prefilter
                     const double incl = warp_incl_scan(wv, lane);
                     const double P = __dadd_rn(carry, incl);
-                    const double r = u01_word(base[q] + cadd);
-                    if (wv > 0.0 && __dmul_rn(r, P) < wv) cand = i + 1;
+                    const uint64_t wd = base[q] + cadd;
+                    if (mix64_yhi(wd) <= thr) {
+                        const double r = u01_word(wd);
+                        if (wv > 0.0 && __dmul_rn(r, P) < wv) cand = i + 1;
+                    }
                     carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
                 }
             }

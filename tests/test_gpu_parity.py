@@ -429,3 +429,22 @@ def test_node2vec_integer_tile_sums_match_oracle(s16, monkeypatch, iscan, wset, 
     np.testing.assert_array_equal(ln, oln)
     np.testing.assert_array_equal(seq, oseq)
     assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()
+
+
+@pytest.mark.parametrize("app", [dict(app="deepwalk", length=40),
+                                 dict(app="ppr", length=40, stop_prob=0.2),
+                                 dict(app="metapath", length=5, schema=(0, 1, 2, 3, 4))])
+def test_rmat_s16_dprs_sampler_matches_oracle(s16, app):
+    """The first-order apps under sampler="dprs" (dprs_warp_exact with its
+    accept prefilter; hub steps use k = 256) against the oracle."""
+    g = s16
+    rs = np.random.default_rng(5)
+    starts = np.concatenate([rs.integers(0, g.vertex_count, 16000),
+                             np.full(500, g.max_degree_vertex())]).astype(np.int64)
+    eng = fw.EngineConfig(replay=True, sampler="dprs")
+    seq, ln, st = _run(g, starts, fw.AppConfig(**app), eng, 3)
+    oseq, oln, ost = oracle.walk(g.offsets, g.targets, g.weights, g.labels, starts, seed=3,
+                                 sampler="dprs", **app)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq, oseq)
+    assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()

@@ -250,6 +250,20 @@ __device__ __forceinline__ double zprs_lane_pass1(const WalkArgs &a, const StepC
     const uint32_t deg = s.deg;
     uint32_t i = j;
     if constexpr (APP != APP_NODE2VEC) {
+        if constexpr (KC != 0 && APP != APP_METAPATH) {
+            // 8 loads in flight per lane (the pass is load-latency-bound)
+            for (; i + 7 * k < deg; i += 8 * k) {
+                float w[8];
+#pragma unroll
+                for (int r = 0; r < 8; r++)
+                    w[r] = a.weighted ? ldg(a.w + s.elo + i + (uint32_t)r * k) : 1.0f;
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    if (staged) stage[i + r * k] = w[r];
+                    lsum = __dadd_rn(lsum, (double)w[r]);
+                }
+            }
+        }
         for (; i + 3 * k < deg; i += 4 * k) {
             double x[4];
             weights4<APP, KC>(a, s, i, k, x);

@@ -251,14 +251,14 @@ __device__ __forceinline__ double zprs_lane_pass1(const WalkArgs &a, const StepC
     uint32_t i = j;
     if constexpr (APP != APP_NODE2VEC) {
         if constexpr (KC != 0 && APP != APP_METAPATH) {
-            // 8 loads in flight per lane (the pass is load-latency-bound)
-            for (; i + 7 * k < deg; i += 8 * k) {
-                float w[8];
+            // 16 loads in flight per lane (the pass is load-latency-bound)
+            for (; i + 15 * k < deg; i += 16 * k) {
+                float w[16];
 #pragma unroll
-                for (int r = 0; r < 8; r++)
+                for (int r = 0; r < 16; r++)
                     w[r] = a.weighted ? ldg(a.w + s.elo + i + (uint32_t)r * k) : 1.0f;
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
+                for (int r = 0; r < 16; r++) {
                     if (staged) stage[i + r * k] = w[r];
                     lsum = __dadd_rn(lsum, (double)w[r]);
                 }

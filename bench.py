@@ -18,10 +18,14 @@ mode, seed 0.  A "step" is one pass of the walk kernel over all V queries.
                threads) on a bounded sample of the same workload (rank 0, N=1).
 
 --impl reference times the reference's CPU implementation the same way
-(rank 0 only; other ranks exit 0).  Multi-GPU (torchrun): the graph is
-generated on rank 0 and broadcast over NCCL (off the timed path), each rank
-walks its own V queries with disjoint global qids (weak scaling, no
-collective on the walk path).
+(rank 0 only; other ranks exit 0).  Multi-GPU (torchrun): the
+graph is generated on rank 0 and broadcast over NCCL (off the timed path);
+ONE query set (one query per vertex) is partitioned into contiguous global-qid
+ranges, one per rank (strong scaling; --scaling weak gives every rank its own
+full query set instead).  No collective runs on the walk path; `value` is all
+ranks' sampled steps over the max-over-ranks device time.  After the timed
+region the path segments are gathered point-to-point to rank 0 (NCCL
+send/recv over NVLink), timed separately (config.gather_ms).
 """
 
 import argparse
@@ -57,12 +61,14 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--nq", type=int, default=0, help="queries (0 = one per vertex)")
-    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                   help="weak: every GPU walks its own full query set (disjoint global qids); "
-                        "strong: one query set partitioned over the GPUs")
-    p.add_argument("--gather", action="store_true",
-                   help="after timing, gather path segments to rank 0 (timed separately)")
+    p.add_argument("--nq", type=int, default=0,
+                   help="queries (0 = one per vertex; 2^24 for scale >= 26, so one step of "
+                        "the s27 workload stays ~17 s on one GPU)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                   help="strong: one query set partitioned over the GPUs (default); "
+                        "weak: every GPU walks its own full query set (disjoint global qids)")
+    p.add_argument("--no-gather", action="store_true",
+                   help="N>1 strong scaling: skip the (separately timed) gather to rank 0")
     p.add_argument("--dump-gather", default=None,
                    help="with --gather: rank 0 saves the gathered paths (.npz) for tests")
     return p.parse_args()
@@ -300,6 +306,9 @@ def bench_ours(args):
     cdev = dev if backend == "nccl" else torch.device("cpu")  # collective tensors
     if world > 1:
         if backend == "nccl":
+            # communicator setup lines (nranks, NVLink/NVLS transport) for the record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
@@ -336,7 +345,7 @@ def bench_ours(args):
             dg = DeviceGraph(V, E_, *arrs[:3], arrs[3] if labels else None, device=local)
     handle = dg.handle(local).ptr
     hub = dg.max_degree_vertex()
-    n_total = args.nq if args.nq else V
+    n_total = args.nq if args.nq else (V if args.scale < 26 else 1 << 24)
     if args.scaling == "strong":
         lo, hi = fwd.partition(n_total, world, rank)
     else:
@@ -380,15 +389,27 @@ def bench_ours(args):
         dist.barrier()
     launch_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     gather_ms = None
-    if world > 1 and args.gather and args.scaling == "strong":
+    if world > 1 and not args.no_gather and args.scaling == "strong":
+        # rank 0 receives every other rank's segment (NCCL send/recv); the
+        # time is the max over ranks of the device time around the exchange
+        src_s, src_l = seq.to(cdev), lens.to(cdev)
         torch.cuda.synchronize()
+        dist.barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
         t_g = time.perf_counter()
-        gathered = fwd.gather_paths(seq.to(cdev), lens.to(cdev), n_total, L, dst=0)
+        g0.record()
+        gathered = fwd.gather_paths(src_s, src_l, n_total, L, dst=0)
+        g1.record()
         torch.cuda.synchronize()
-        gather_ms = 1000 * (time.perf_counter() - t_g)
+        gm = torch.tensor([max(g0.elapsed_time(g1), 1000 * (time.perf_counter() - t_g))],
+                          dtype=torch.float64, device=cdev)
+        dist.all_reduce(gm, op=dist.ReduceOp.MAX)
+        gather_ms = float(gm.item())
         if args.dump_gather and rank == 0:  # consumed by tests/test_gpu_parity.py
             np.savez(args.dump_gather, seq=gathered[0].cpu().numpy().view(np.uint32),
                      lens=gathered[1].cpu().numpy().view(np.uint32))
+        del gathered, src_s, src_l
     my_ms = sum(launch_ms)
     st = stats.cpu().numpy()
     tail = {"last_launch_ms": launch_ms[-1],
@@ -398,7 +419,11 @@ def bench_ours(args):
     alg_bytes = int(st[7])
     t = torch.tensor([my_ms], dtype=torch.float64, device=cdev)
     tot = torch.tensor([sampled], dtype=torch.int64, device=cdev)
+    per_rank_ms = [my_ms]
     if world > 1:
+        allt = [torch.zeros(1, dtype=torch.float64, device=cdev) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank_ms = [float(x.item()) for x in allt]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     elapsed_ms = float(t.item())
@@ -465,6 +490,9 @@ def bench_ours(args):
                        "vertices": V, "csr_entries": E_, "queries_per_gpu": n,
                        "replicate_s": None if world == 1 else round(t_rep, 3),
                        "gather_ms": gather_ms,
+                       "gather_bytes": (n_total * L * 4 + n_total * 4) if gather_ms else None,
+                       "per_rank_walk_ms": [round(x, 3) for x in per_rank_ms],
+                       "total_queries": n_total if args.scaling == "strong" else n_total * world,
                        "backend": backend if world > 1 else None,
                        "parallelism": f"replicated graph, qids partitioned x{world}",
                        "l2": "inputs larger than L2 (graph + result pool > 126 MB), no flush",

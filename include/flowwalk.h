@@ -94,6 +94,12 @@ typedef struct {
     int32_t d2h_pieces;     /* fw_walk: result pieces copied back while the walk ran
                                (0: copied after the kernel) */
     double tail_ms;         /* first to last warp exit: the load-imbalance tail */
+    int64_t aux_bytes;      /* device scratch the engine holds besides the graph and the
+                               result buffers (cursor slots, counters, piece counters,
+                               schema copies): the reference's AllocationMeter total
+                               (engine.py:35-48), independent of d_max and |Q| */
+    int64_t aux_allocations;
+    int64_t scratch_bytes;  /* fw_walk: device result/start staging in use */
 } fw_stats;
 
 typedef struct {
@@ -102,31 +108,54 @@ typedef struct {
     float max_weight;
     int32_t min_weight_lowbit_exp; /* min over w>0 of exponent of w's lowest set bit */
     int32_t has_labels;
-    int32_t reserved;
+    int32_t bad_weights;   /* some weight is negative or non-finite */
+    int32_t sorted_lists;  /* every neighbour list is non-decreasing (Node2Vec needs it) */
+    int32_t pad_;
 } fw_graph_info;
 
 const char *fw_last_error(void);
 int fw_device_count(int *out);
 
-/* Upload host CSR arrays once (pinned staging); labels may be NULL. */
+/* Upload host CSR arrays once (pinned staging); labels may be NULL.
+ * Both constructors check the CSR on the device before returning a handle:
+ * offsets[0] == 0, offsets[V] == E, offsets non-decreasing and every target
+ * < V (FW_EVALIDATION otherwise, the reference's Graph.validate,
+ * graph.py:70-81); per-vertex sortedness is recorded in fw_graph_info and
+ * required by Node2Vec walks (its membership test binary-searches N(prev),
+ * _kernels.py:293-306). */
 int fw_graph_create(const int64_t *offsets, const uint32_t *targets, const float *weights,
                     const uint8_t *labels_or_null, uint64_t vertex_count, uint64_t edge_count,
                     int device, fw_graph **out);
-/* Wrap device-resident CSR arrays already on `device` (borrowed, not freed). */
+/* Wrap device-resident CSR arrays already on `device` (borrowed, not freed).
+ * Contract: d_targets and d_weights stay readable 16 bytes past element E-1
+ * (the walk kernel loads 16-byte tiles). */
 int fw_graph_create_device(const int64_t *d_offsets, const uint32_t *d_targets,
                            const float *d_weights, const uint8_t *d_labels_or_null,
                            uint64_t vertex_count, uint64_t edge_count, int device,
                            fw_graph **out);
+/* Replica of a resident graph on another device by device-to-device peer
+ * copies (the multi-GPU fan-out of SURVEY §8(e)); the new handle owns its
+ * arrays.  Works for device == src's device too (a second private copy). */
+int fw_graph_replicate(fw_graph *src, int device, fw_graph **out);
 int fw_graph_destroy(fw_graph *g);
+/* Device scratch cap for fw_walk's result/start staging (bytes; 0 = auto:
+ * 90% of the device's free memory at call time).  Reference analogue: the
+ * Eq. 3 memory budget (engine.py:90-105) applied to device memory. */
+int fw_graph_set_scratch_limit(fw_graph *g, uint64_t bytes);
 int fw_graph_info_get(fw_graph *g, fw_graph_info *out);
 
 /* Host-buffer walk: H2D starts, walk, D2H sequences (n*length u32, sentinel
- * padded) and lengths (n u32).  Stats are written (not accumulated). */
+ * padded) and lengths (n u32).  Stats are written (not accumulated).  When
+ * n * (length + 3) * 4 bytes exceed the handle's scratch limit the queries are
+ * walked in sub-launches over two alternating device buffers, each one's D2H
+ * overlapping the next launch (PAPER.md:394-400 ping-pong). */
 int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t base_qid,
             const fw_app *app, const fw_engine *eng, uint64_t seed,
             uint32_t *out_seq, uint32_t *out_len, fw_stats *stats);
 
 /* Device-buffer walk, asynchronous on `stream` (a cudaStream_t, may be NULL).
+ * Launches on different streams may overlap: each takes its own work-queue
+ * cursor slot, and a slot is reused only after its previous kernel finished.
  * d_stats (int64[10], device) is ACCUMULATED: steps, edges, collectives, draws,
  * small, large, sampled_steps, alg_bytes; words 8/9 take the max of the warps'
  * exit time and of its complement (%globaltimer ns, zero them per launch). */

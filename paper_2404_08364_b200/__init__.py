@@ -10,7 +10,7 @@ reference are out of scope.
 
 from .apps import APP_IDS, APPS, AppConfig, WalkQuery
 from .engine import (AllocationMeter, BatchResult, DeviceGraph, EngineConfig, GlobalPool,
-                     RunStats, batch_size, read_result_file, run, run_batches,
+                     RunStats, batch_size, evict, read_result_file, run, run_batches,
                      throughput_report, to_device, write_result_file)
 from .errors import (CapacityError, ConfigError, FormatError, ParseError,
                      RejectionExhausted, ReswalkError, ValidationError)
@@ -23,7 +23,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "APPS", "APP_IDS", "AppConfig", "WalkQuery", "AllocationMeter", "BatchResult",
-    "DeviceGraph", "EngineConfig", "GlobalPool", "RunStats", "batch_size",
+    "DeviceGraph", "EngineConfig", "GlobalPool", "RunStats", "batch_size", "evict",
     "read_result_file", "run", "run_batches", "throughput_report", "to_device",
     "write_result_file", "CapacityError", "ConfigError", "FormatError", "ParseError",
     "RejectionExhausted", "ReswalkError", "ValidationError", "EdgeList", "Graph",

@@ -38,17 +38,19 @@ class FwStats(ctypes.Structure):
         ("kernel_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
         ("exact_order", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32), ("d2h_pieces", ctypes.c_int32),
-        ("tail_ms", ctypes.c_double)]
+        ("tail_ms", ctypes.c_double), ("aux_bytes", ctypes.c_int64),
+        ("aux_allocations", ctypes.c_int64), ("scratch_bytes", ctypes.c_int64)]
 
 
 class FwGraphInfo(ctypes.Structure):
     _fields_ = [("max_degree", ctypes.c_int64), ("max_degree_vertex", ctypes.c_int64),
                 ("max_weight", ctypes.c_float), ("min_weight_lowbit_exp", ctypes.c_int32),
-                ("has_labels", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("has_labels", ctypes.c_int32), ("bad_weights", ctypes.c_int32),
+                ("sorted_lists", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 EXPORTS = ("fw_last_error", "fw_device_count", "fw_graph_create", "fw_graph_create_device",
-           "fw_graph_destroy", "fw_graph_info_get", "fw_walk", "fw_walk_device",
+           "fw_graph_replicate", "fw_graph_destroy", "fw_graph_set_scratch_limit", "fw_graph_info_get", "fw_walk", "fw_walk_device",
            "fw_validate_device", "fw_sampler_trials_device", "fw_rmat_edges_device",
            "fw_synth_weights_device", "fw_synth_labels_device")
 
@@ -71,7 +73,9 @@ def load(path=LIB_PATH):
         "fw_device_count": ([P], I32),
         "fw_graph_create": ([P, P, P, P, U64, U64, I32, P], I32),
         "fw_graph_create_device": ([P, P, P, P, U64, U64, I32, P], I32),
+        "fw_graph_replicate": ([P, I32, P], I32),
         "fw_graph_destroy": ([P], I32),
+        "fw_graph_set_scratch_limit": ([P, U64], I32),
         "fw_graph_info_get": ([P, P], I32),
         "fw_walk": ([P, P, U64, U64, P, P, U64, P, P, P], I32),
         "fw_walk_device": ([P, P, U64, U64, P, P, U64, P, P, P, P], I32),
@@ -89,12 +93,15 @@ def load(path=LIB_PATH):
     return lib
 
 
-def check(rc):
-    """Map a C status code onto the reference's exception classes."""
+def check(rc, msg=None):
+    """Map a C status code onto the reference's exception classes.  ``msg``:
+    fw_last_error() as read on the thread that made the failing call (the
+    message is thread-local)."""
     if rc == FW_OK:
         return
     from .errors import ConfigError, ValidationError
-    msg = load().fw_last_error().decode(errors="replace")
+    if msg is None:
+        msg = load().fw_last_error().decode(errors="replace")
     if rc == FW_EVALIDATION:
         raise ValidationError(msg)
     if rc == FW_ECONFIG:

@@ -75,16 +75,33 @@ struct fw_graph {
     fw_graph_info info{};
     unsigned long long *queues = nullptr;  // ring of per-launch cursors
     unsigned call_counter = 0;
+    // a cursor slot (and its schema copy) is reused only after the kernel
+    // that last used it has finished, whatever stream either runs on
+    cudaEvent_t slot_ev[kQueueRing] = {};
+    bool slot_used[kQueueRing] = {};
     std::mutex mu;
     std::mutex host_mu;  // serialises fw_walk's host-buffer scratch
-    // host-buffer walk scratch (grow-only)
-    DevBuf starts, seq, len, stats, schema, done;
+    // host-buffer walk scratch (grow-only); [1] only for sub-launched walks
+    DevBuf starts[2], seq[2], len[2], stats, done;
     std::vector<DevBuf> schema_ring;
+    uint64_t scratch_limit = 0;  // bytes, 0 = auto
     int sm_count = 0;
     // fw_walk's streams and events, created on first use and kept (creating
     // them per call cost tens of microseconds against millisecond walks)
     cudaStream_t walk_st = nullptr, copy_st = nullptr;
     cudaEvent_t ev[6] = {};
+    cudaEvent_t buf_free[2] = {};  // sub-launch ping-pong: buffer's D2H done
+
+    int64_t aux_bytes() const {  // the engine's own scratch (AllocationMeter analogue)
+        int64_t b = kQueueRing * sizeof(unsigned long long) + stats.cap + done.cap;
+        for (const DevBuf &x : schema_ring) b += x.cap;
+        return b;
+    }
+    int64_t aux_allocations() const {
+        int64_t n = 1 + (stats.cap ? 1 : 0) + (done.cap ? 1 : 0);
+        for (const DevBuf &x : schema_ring) n += x.cap ? 1 : 0;
+        return n;
+    }
 };
 
 extern "C" const char *fw_last_error(void) { return g_err.c_str(); }
@@ -145,7 +162,76 @@ __global__ void k_weight_profile(const float *__restrict__ w, uint64_t E, int *m
     }
 }
 
+// CSR checks (reference Graph.validate, graph.py:70-81): offsets
+// non-decreasing, targets < V; per-vertex sortedness is recorded (the
+// reference accepts unsorted lists, but its Node2Vec membership test is a
+// binary search over N(prev), _kernels.py:293-306, which our window tables
+// reproduce only for sorted lists).  Flags: 1 = offsets decrease, 2 = target
+// out of range, 4 = some list unsorted.
+__global__ void k_check_offsets(const int64_t *__restrict__ off, uint64_t V, uint64_t E,
+                                uint32_t *bounds, int *flags) {
+    int f = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t a = off[v], b = off[v + 1];
+        if (b < a || a < 0 || b > (int64_t)E) { f |= 1; continue; }
+        if (b > a) atomicOr(bounds + (a >> 5), 1u << (a & 31));  // a list starts at a
+    }
+    if (f) atomicOr(flags, f);
+}
+
+__global__ void k_check_targets(const uint32_t *__restrict__ tgt, uint64_t E, uint64_t V,
+                                const uint32_t *__restrict__ bounds, int *flags) {
+    int f = 0;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = tgt[e];
+        if ((uint64_t)t >= V) f |= 2;
+        if (e + 1 < E && t > tgt[e + 1] && !((bounds[(e + 1) >> 5] >> ((e + 1) & 31)) & 1)) f |= 4;
+    }
+    f |= __shfl_xor_sync(FULL, f, 16);
+    f |= __shfl_xor_sync(FULL, f, 8);
+    f |= __shfl_xor_sync(FULL, f, 4);
+    f |= __shfl_xor_sync(FULL, f, 2);
+    f |= __shfl_xor_sync(FULL, f, 1);
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+static int check_csr(fw_graph *g) {
+    int64_t ends[2] = {0, 0};
+    CU(cudaMemcpy(&ends[0], g->off, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&ends[1], g->off + g->V, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (ends[0] != 0 || (uint64_t)ends[1] != g->E)
+        return set_err(FW_EVALIDATION, "offsets must start at 0 and end at edge_count");
+    if (g->E && (!g->tgt || !g->w))
+        return set_err(FW_EVALIDATION, "null targets or weights for a non-empty graph");
+    uint32_t *bounds = nullptr;
+    int *flags = nullptr;
+    const size_t nw = (g->E + 1 + 31) / 32;
+    CU(cudaMalloc(&bounds, nw * sizeof(uint32_t)));
+    CU(cudaMalloc(&flags, sizeof(int)));
+    cudaMemset(bounds, 0, nw * sizeof(uint32_t));
+    cudaMemset(flags, 0, sizeof(int));
+    const int grid = g->sm_count * 8;
+    if (g->V) k_check_offsets<<<grid, 256>>>(g->off, g->V, g->E, bounds, flags);
+    int f = 0;
+    cudaError_t e = cudaMemcpy(&f, flags, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && !(f & 1) && g->E) {
+        k_check_targets<<<grid, 256>>>(g->tgt, g->E, g->V, bounds, flags);
+        e = cudaMemcpy(&f, flags, sizeof(int), cudaMemcpyDeviceToHost);
+    }
+    cudaFree(bounds);
+    cudaFree(flags);
+    CU(e);
+    if (f & 1) return set_err(FW_EVALIDATION, "offsets must be non-decreasing");
+    if (f & 2) return set_err(FW_EVALIDATION, "target id out of range");
+    g->info.sorted_lists = (f & 4) ? 0 : 1;
+    return FW_OK;
+}
+
 static int profile_graph(fw_graph *g) {
+    int rc = check_csr(g);
+    if (rc) return rc;
     unsigned long long *d_deg;
     int *d_i;
     CU(cudaMalloc(&d_deg, sizeof(unsigned long long)));
@@ -171,7 +257,7 @@ static int profile_graph(fw_graph *g) {
     memcpy(&mw, &mb, sizeof(mw));
     g->info.max_weight = mw;
     g->info.has_labels = g->lab != nullptr;
-    g->info.reserved = res[2];  // non-finite / negative weight flag
+    g->info.bad_weights = res[2];  // non-finite / negative weight flag
     return FW_OK;
 }
 
@@ -271,6 +357,52 @@ extern "C" int fw_graph_create_device(const int64_t *d_off, const uint32_t *d_tg
     return FW_OK;
 }
 
+// Replica of a resident CSR on another device: device-to-device peer copies
+// (NVLink on NVSwitch systems; staged by the driver when peers are not
+// enabled), no host round trip and no re-validation.
+extern "C" int fw_graph_replicate(fw_graph *src, int device, fw_graph **out) {
+    if (!src || !out) return set_err(FW_EVALIDATION, "null handle");
+    fw_graph *g = new fw_graph();
+    int rc = graph_common_init(g, device);
+    if (rc) { delete g; return rc; }
+    g->V = src->V;
+    g->E = src->E;
+    g->owned = true;
+    g->info = src->info;
+    const uint64_t V = g->V, E = g->E;
+    auto fail = [&](int code) {
+        fw_graph_destroy(g);
+        return code;
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&g->off, (V + 1) * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&g->tgt, (E + 4) * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&g->w, (E + 4) * sizeof(float))) != cudaSuccess ||
+        (src->lab && (e = cudaMalloc(&g->lab, std::max<uint64_t>(E, 1))) != cudaSuccess))
+        return fail(set_err(FW_ENOMEM, "replica allocation: %s", cudaGetErrorString(e)));
+    int can = 0;
+    if (device != src->device && cudaDeviceCanAccessPeer(&can, device, src->device) == cudaSuccess &&
+        can) {
+        e = cudaDeviceEnablePeerAccess(src->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    }
+    cudaStream_t st;
+    if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(set_err(FW_ECUDA, "stream: %s", cudaGetErrorString(e)));
+    e = cudaMemcpyPeerAsync(g->off, device, src->off, src->device, (V + 1) * sizeof(int64_t), st);
+    if (e == cudaSuccess && E)
+        e = cudaMemcpyPeerAsync(g->tgt, device, src->tgt, src->device, E * sizeof(uint32_t), st);
+    if (e == cudaSuccess && E)
+        e = cudaMemcpyPeerAsync(g->w, device, src->w, src->device, E * sizeof(float), st);
+    if (e == cudaSuccess && E && src->lab)
+        e = cudaMemcpyPeerAsync(g->lab, device, src->lab, src->device, E, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (e != cudaSuccess) return fail(set_err(FW_ECUDA, "peer copy: %s", cudaGetErrorString(e)));
+    *out = g;
+    return FW_OK;
+}
+
 extern "C" int fw_graph_destroy(fw_graph *g) {
     if (!g) return FW_OK;
     cudaSetDevice(g->device);
@@ -281,12 +413,16 @@ extern "C" int fw_graph_destroy(fw_graph *g) {
         if (g->lab) cudaFree(g->lab);
     }
     if (g->queues) cudaFree(g->queues);
-    g->starts.release();
-    g->seq.release();
-    g->len.release();
+    for (int i = 0; i < 2; i++) {
+        g->starts[i].release();
+        g->seq[i].release();
+        g->len[i].release();
+        if (g->buf_free[i]) cudaEventDestroy(g->buf_free[i]);
+    }
     g->stats.release();
-    g->schema.release();
     g->done.release();
+    for (int i = 0; i < kQueueRing; i++)
+        if (g->slot_ev[i]) cudaEventDestroy(g->slot_ev[i]);
     if (g->walk_st) {
         for (cudaEvent_t e : g->ev) cudaEventDestroy(e);
         cudaStreamDestroy(g->walk_st);
@@ -294,6 +430,13 @@ extern "C" int fw_graph_destroy(fw_graph *g) {
     }
     for (auto &b : g->schema_ring) b.release();
     delete g;
+    return FW_OK;
+}
+
+extern "C" int fw_graph_set_scratch_limit(fw_graph *g, uint64_t bytes) {
+    if (!g) return set_err(FW_EVALIDATION, "null handle");
+    std::lock_guard<std::mutex> lk(g->host_mu);
+    g->scratch_limit = bytes;
     return FW_OK;
 }
 
@@ -311,7 +454,7 @@ extern "C" int fw_graph_info_get(fw_graph *g, fw_graph_info *out) {
 // ---------------------------------------------------------------------------
 static bool exact_order_ok(const fw_graph_info &gi, const fw_app &app, long *g_out = nullptr,
                            double *xmax_out = nullptr) {
-    if (gi.reserved) return false;  // non-finite or negative weights: be literal
+    if (gi.bad_weights) return false;  // non-finite or negative weights: be literal
     std::vector<double> F{1.0};
     if (app.app_id == FW_APP_NODE2VEC) {
         F.push_back(app.inv_a);
@@ -360,6 +503,9 @@ static int check_cfg(fw_graph *g, const fw_app *app, const fw_engine *eng) {
     if (eng->d_t < 1) return set_err(FW_ECONFIG, "degree threshold must be >= 1");
     if (eng->sampler_id != FW_SAMPLER_ZPRS && eng->sampler_id != FW_SAMPLER_DPRS)
         return set_err(FW_ECONFIG, "unknown sampler id");
+    if (app->app_id == FW_APP_NODE2VEC && !g->info.sorted_lists)
+        return set_err(FW_EVALIDATION,
+                       "node2vec needs every neighbour list sorted (build_csr order)");
     return FW_OK;
 }
 
@@ -401,7 +547,7 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         if ((double)f < wm) f = std::nextafter(f, INFINITY);
         // inf: prefilter off.  Negative or non-finite weights (reserved) let
         // the running prefix shrink, which the prefilter's bound assumes away.
-        const bool lit = app->weighted && g->info.reserved;
+        const bool lit = app->weighted && g->info.bad_weights;
         a.accept_wmax = (std::isfinite(f) && f <= 1e37f && !lit) ? f : INFINITY;
     }
     {   // fp32 factor path: 1/a, 1/b = 2^k and every w * 2^k exact in fp32
@@ -416,7 +562,7 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
                   pow2_exp(app->inv_b, &kb) && std::abs(ka) <= 16 && std::abs(kb) <= 16;
         if (ok && app->weighted) {
             const int kmin = std::min({0, ka, kb}), kmax = std::max({0, ka, kb});
-            ok = !g->info.reserved &&
+            ok = !g->info.bad_weights &&
                  (!(g->info.max_weight > 0.0f) ||
                   ((long)g->info.min_weight_lowbit_exp + kmin >= -149 &&
                    std::ldexp((double)g->info.max_weight, kmax) <= (double)FLT_MAX));
@@ -453,21 +599,28 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     a.stats = (long long *)d_stats;
     a.done = d_done;
     a.piece_q = piece_q ? piece_q : 1;
-    unsigned slot;
-    {
-        std::lock_guard<std::mutex> lk(g->mu);
-        slot = g->call_counter++ % kQueueRing;
-        if (g->schema_ring.empty()) g->schema_ring.resize(kQueueRing);
-    }
+    std::unique_lock<std::mutex> lk(g->mu);  // held until the slot's event is recorded
+    const unsigned slot = g->call_counter++ % kQueueRing;
+    if (g->schema_ring.empty()) g->schema_ring.resize(kQueueRing);
+    if (!g->slot_ev[slot]) CU(cudaEventCreateWithFlags(&g->slot_ev[slot], cudaEventDisableTiming));
+    // the slot's previous kernel (possibly on another stream) must be done
+    // before its cursor is re-zeroed or its schema copy overwritten
+    if (g->slot_used[slot]) CU(cudaStreamWaitEvent(stream, g->slot_ev[slot], 0));
     a.queue = g->queues + slot;
     CU(cudaMemsetAsync(a.queue, 0, sizeof(unsigned long long), stream));
     if (app->app_id == FW_APP_METAPATH) {
-        DevBuf &sb = g->schema_ring[slot];
-        CU(sb.reserve(app->schema_len * sizeof(int64_t)));
-        CU(cudaMemcpyAsync(sb.p, app->schema, app->schema_len * sizeof(int64_t),
-                           cudaMemcpyHostToDevice, stream));
-        a.schema = (const int64_t *)sb.p;
         a.schema_len = app->schema_len;
+        if (app->schema_len <= kSchemaInline) {  // in the kernel arguments: no device copy
+            for (uint32_t i = 0; i < app->schema_len; i++) a.schema_inline[i] = app->schema[i];
+            a.schema = nullptr;
+        } else {
+            DevBuf &sb = g->schema_ring[slot];
+            if (sb.cap < app->schema_len * sizeof(int64_t)) CU(cudaStreamSynchronize(stream));
+            CU(sb.reserve(app->schema_len * sizeof(int64_t)));
+            CU(cudaMemcpyAsync(sb.p, app->schema, app->schema_len * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, stream));
+            a.schema = (const int64_t *)sb.p;
+        }
     }
     const int occ = std::max(1, walk_occupancy(app->app_id, eng->sampler_id, exact));
     const uint64_t warps_needed = n;
@@ -476,6 +629,8 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     if (grid > max_useful) grid = max_useful;
     if (grid_out) *grid_out = (int)grid;
     CU(launch_walk(a, app->app_id, eng->sampler_id, exact, (int)grid, stream));
+    CU(cudaEventRecord(g->slot_ev[slot], stream));
+    g->slot_used[slot] = true;
     return FW_OK;
 }
 
@@ -520,14 +675,34 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     CU(cudaSetDevice(g->device));
     std::lock_guard<std::mutex> lk(g->host_mu);
     const uint64_t L = app->length;
-    CU(g->starts.reserve(std::max<uint64_t>(n, 1) * sizeof(int64_t)));
-    CU(g->seq.reserve(std::max<uint64_t>(n * L, 1) * sizeof(uint32_t)));
-    CU(g->len.reserve(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+    // Device staging per query: the path row, its length and its start.
+    // Above the scratch limit the walk runs in sub-launches over two
+    // alternating buffers (Eq. 3's ping-pong, applied to
+    // device memory); each buffer's D2H overlaps the next sub-launch.
+    const uint64_t per_q = L * sizeof(uint32_t) + sizeof(uint32_t) + sizeof(int64_t);
+    uint64_t limit = g->scratch_limit;
+    if (!limit) {
+        size_t fr = 0, tot = 0;
+        CU(cudaMemGetInfo(&fr, &tot));
+        uint64_t held = 0;
+        for (int i = 0; i < 2; i++) held += g->starts[i].cap + g->seq[i].cap + g->len[i].cap;
+        limit = (uint64_t)((double)(fr + held) * 0.9);
+    }
+    const uint64_t rows_cap = std::max<uint64_t>(limit / per_q, 2);
+    const bool single = n <= rows_cap;
+    const uint64_t chunk = single ? std::max<uint64_t>(n, 1) : rows_cap / 2;
+    const uint64_t nsub = single ? 1 : (n + chunk - 1) / chunk;
+    for (int i = 0; i < (nsub > 1 ? 2 : 1); i++) {
+        CU(g->starts[i].reserve(chunk * sizeof(int64_t)));
+        CU(g->seq[i].reserve(chunk * L * sizeof(uint32_t)));
+        CU(g->len[i].reserve(chunk * sizeof(uint32_t)));
+    }
     CU(g->stats.reserve(ST_WORDS * sizeof(int64_t)));
-    // Pieces of the result are copied back on a second stream as soon as all
-    // of a piece's queries are done (the kernel counts them; the copy stream
-    // waits on the count), so only the last piece's D2H trails the walk.
-    WaitValue32Fn wv = n >= kD2hMinQueries ? wait_value32() : nullptr;
+    // Single launch: pieces of the result are copied back on a second stream
+    // as soon as all of a piece's queries are done (the kernel counts them;
+    // the copy stream waits on the count), so only the last piece's D2H
+    // trails the walk.
+    WaitValue32Fn wv = single && n >= kD2hMinQueries ? wait_value32() : nullptr;
     const uint64_t P = wv ? kD2hPieces : 0;
     const uint64_t piece_q = P ? (n + P - 1) / P : 0;
     if (P) CU(g->done.reserve(P * sizeof(unsigned)));
@@ -537,55 +712,85 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         for (int i = 0; i < 4; i++) CU(cudaEventCreate(&g->ev[i]));
         CU(cudaEventCreateWithFlags(&g->ev[4], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&g->ev[5], cudaEventDisableTiming));
+        for (int i = 0; i < 2; i++) CU(cudaEventCreateWithFlags(&g->buf_free[i], cudaEventDisableTiming));
     }
     cudaStream_t st = g->walk_st, cs = g->copy_st;
     cudaEvent_t e0 = g->ev[0], e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3], ez = g->ev[4];
     cudaEventRecord(e0, st);
     cudaMemsetAsync(g->stats.p, 0, ST_WORDS * sizeof(int64_t), st);
-    if (P) cudaMemsetAsync(g->done.p, 0, P * sizeof(unsigned), st);
-    if (n) cudaMemcpyAsync(g->starts.p, starts, n * sizeof(int64_t), cudaMemcpyHostToDevice, st);
-    cudaEventRecord(e1, st);
-    cudaEventRecord(ez, st);  // the counters are zero from here on
     bool exact = false;
-    int grid = 0;
-    rc = launch(g, (const int64_t *)g->starts.p, n, base_qid, app, eng, seed,
-                (uint32_t *)g->seq.p, (uint32_t *)g->len.p, (int64_t *)g->stats.p, st, &exact,
-                &grid, P ? (unsigned *)g->done.p : nullptr, piece_q);
-    cudaEventRecord(e2, st);
-    int64_t hst[ST_WORDS] = {0};
-    int pieces = 0;
-    if (!rc) {
-        if (P) {
-            cudaStreamWaitEvent(cs, ez, 0);
-            for (uint64_t i = 0; i < P && i * piece_q < n; i++) {
-                const uint64_t q0 = i * piece_q, cnt = std::min(piece_q, n - q0);
-                const CUdeviceptr dc = (CUdeviceptr)((unsigned *)g->done.p + i);
-                if (wv(cs, dc, (cuuint32_t)cnt, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
-                    rc = set_err(FW_ECUDA, "cuStreamWaitValue32 failed");
-                    break;
+    int grid = 0, pieces = 0, launches = 0;
+    if (single) {
+        if (P) cudaMemsetAsync(g->done.p, 0, P * sizeof(unsigned), st);
+        if (n) cudaMemcpyAsync(g->starts[0].p, starts, n * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+        cudaEventRecord(e1, st);
+        cudaEventRecord(ez, st);  // the counters are zero from here on
+        rc = launch(g, (const int64_t *)g->starts[0].p, n, base_qid, app, eng, seed,
+                    (uint32_t *)g->seq[0].p, (uint32_t *)g->len[0].p, (int64_t *)g->stats.p, st,
+                    &exact, &grid, P ? (unsigned *)g->done.p : nullptr, piece_q);
+        launches = n ? 1 : 0;
+        cudaEventRecord(e2, st);
+        if (!rc) {
+            if (P) {
+                cudaStreamWaitEvent(cs, ez, 0);
+                for (uint64_t i = 0; i < P && i * piece_q < n; i++) {
+                    const uint64_t q0 = i * piece_q, cnt = std::min(piece_q, n - q0);
+                    const CUdeviceptr dc = (CUdeviceptr)((unsigned *)g->done.p + i);
+                    if (wv(cs, dc, (cuuint32_t)cnt, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+                        rc = set_err(FW_ECUDA, "cuStreamWaitValue32 failed");
+                        break;
+                    }
+                    cudaMemcpyAsync(out_seq + q0 * L, (uint32_t *)g->seq[0].p + q0 * L,
+                                    cnt * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, cs);
+                    cudaMemcpyAsync(out_len + q0, (uint32_t *)g->len[0].p + q0,
+                                    cnt * sizeof(uint32_t), cudaMemcpyDeviceToHost, cs);
+                    pieces++;
                 }
-                cudaMemcpyAsync(out_seq + q0 * L, (uint32_t *)g->seq.p + q0 * L,
-                                cnt * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, cs);
-                cudaMemcpyAsync(out_len + q0, (uint32_t *)g->len.p + q0, cnt * sizeof(uint32_t),
-                                cudaMemcpyDeviceToHost, cs);
-                pieces++;
+                cudaStreamWaitEvent(st, e2, 0);
+            } else if (n) {
+                cudaMemcpyAsync(out_seq, g->seq[0].p, n * L * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(out_len, g->len[0].p, n * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, st);
             }
-            cudaStreamWaitEvent(st, e2, 0);
-        } else if (n) {
-            cudaMemcpyAsync(out_seq, g->seq.p, n * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
-            cudaMemcpyAsync(out_len, g->len.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
         }
+    } else {
+        cudaEventRecord(e1, st);
+        for (uint64_t j = 0; j < nsub && !rc; j++) {
+            const int b = (int)(j & 1);
+            const uint64_t q0 = j * chunk, cnt = std::min(chunk, n - q0);
+            if (j >= 2) cudaStreamWaitEvent(st, g->buf_free[b], 0);  // D2H of sub-launch j-2 done
+            cudaMemcpyAsync(g->starts[b].p, starts + q0, cnt * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, st);
+            rc = launch(g, (const int64_t *)g->starts[b].p, cnt, base_qid + q0, app, eng, seed,
+                        (uint32_t *)g->seq[b].p, (uint32_t *)g->len[b].p,
+                        (int64_t *)g->stats.p, st, &exact, &grid);
+            if (rc) break;
+            launches++;
+            cudaEventRecord(ez, st);
+            cudaStreamWaitEvent(cs, ez, 0);
+            cudaMemcpyAsync(out_seq + q0 * L, g->seq[b].p, cnt * L * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, cs);
+            cudaMemcpyAsync(out_len + q0, g->len[b].p, cnt * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, cs);
+            cudaEventRecord(g->buf_free[b], cs);
+        }
+        cudaEventRecord(e2, st);
+    }
+    int64_t hst[ST_WORDS] = {0};
+    if (!rc) {
         cudaMemcpyAsync(hst, g->stats.p, sizeof(hst), cudaMemcpyDeviceToHost, st);
-        if (P) {  // the end event covers both streams
+        if (P || !single) {  // the end event covers both streams
             cudaEventRecord(g->ev[5], cs);
             cudaStreamWaitEvent(st, g->ev[5], 0);
         }
         cudaEventRecord(e3, st);
-        cudaError_t ce = cudaStreamSynchronize(st);
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize(cs);
-        if (ce != cudaSuccess && !rc)
-            rc = set_err(FW_ECUDA, "walk failed: %s", cudaGetErrorString(ce));
     }
+    // always drain both streams: no copy may still target the caller's buffers
+    cudaError_t ce = cudaStreamSynchronize(st);
+    const cudaError_t ce2 = cudaStreamSynchronize(cs);
+    if (ce == cudaSuccess) ce = ce2;
+    if (ce != cudaSuccess && !rc) rc = set_err(FW_ECUDA, "walk failed: %s", cudaGetErrorString(ce));
     if (!rc && stats) {
         float kms = 0.f, tms = 0.f;
         cudaEventElapsedTime(&kms, e1, e2);
@@ -602,10 +807,15 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         stats->total_ms = tms;
         stats->exact_order = exact;
         stats->grid_ctas = grid;
-        stats->kernel_launches = n ? 1 : 0;
+        stats->kernel_launches = launches;
         stats->d2h_pieces = pieces;
         const uint64_t last = (uint64_t)hst[ST_T_LAST], first = ~(uint64_t)hst[ST_T_FIRST_NEG];
         stats->tail_ms = (n && last >= first) ? (double)(last - first) * 1e-6 : 0.0;
+        stats->aux_bytes = g->aux_bytes();
+        stats->aux_allocations = g->aux_allocations();
+        int64_t sb = 0;
+        for (int i = 0; i < 2; i++) sb += g->starts[i].cap + g->seq[i].cap + g->len[i].cap;
+        stats->scratch_bytes = sb;
     }
     return rc;
 }

@@ -1239,7 +1239,7 @@ __device__ __forceinline__ void stat_add(unsigned long long *st, int idx, long l
 // ---------------------------------------------------------------------------
 template <int APP, int SAMPLER, bool EXACT>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks(APP))
-walk_kernel(const WalkArgs a) {
+walk_kernel(const __grid_constant__ WalkArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t woff = (threadIdx.x >> 5) * warp_words(APP);
     // per-warp RunStats counters live in shared memory (registers are the
@@ -1281,7 +1281,7 @@ walk_kernel(const WalkArgs a) {
             if (s.deg == 0) break;
             if constexpr (APP == APP_METAPATH) {
                 if (step >= a.schema_len) break;
-                s.want = ldg(a.schema + step);
+                s.want = a.schema ? ldg(a.schema + step) : a.schema_inline[step];
             }
             if constexpr (APP == APP_NODE2VEC) {
                 if (s.prev >= 0) {  // N(prev) = the previous step's N(cur)

@@ -48,7 +48,8 @@ struct WalkArgs {
     uint32_t *out_len;    // n
     uint32_t L;
     uint32_t schema_len;
-    const int64_t *schema;  // device copy
+    const int64_t *schema;  // device copy, or null: schema_inline holds it
+    int64_t schema_inline[16];
     int32_t weighted;
     double stop_prob, inv_a, inv_b;
     double fac[4];  // node2vec factor by 2*is_prev + is_member: {1/b, 1, 1/a, 1/a}
@@ -75,6 +76,8 @@ struct WalkArgs {
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };
+
+constexpr uint32_t kSchemaInline = 16;  // metapath schemas up to this length ride in the args
 
 cudaError_t launch_walk(const WalkArgs &a, int app, int sampler, bool exact, int grid,
                         cudaStream_t stream);

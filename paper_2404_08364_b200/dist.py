@@ -7,8 +7,8 @@ There are two off-path exchanges:
 
   * replicate_csr: one source rank's CSR arrays are broadcast to all ranks
     (NCCL over NVLink for cuda tensors; gloo for CPU tensors in tests);
-  * gather_paths: the per-rank (sequences, lengths) segments are
-    concatenated on the destination rank in qid order.
+  * gather_paths: the per-rank (sequences, lengths) segments are sent
+    point-to-point to the destination rank, in qid order.
 
 One process per GPU (torchrun); torch.distributed is plumbing only.
 """
@@ -41,26 +41,32 @@ def replicate_csr(arrays, shapes_dtypes, src=0, device=None):
 
 
 def gather_paths(seq, lens, n_total, L, dst=0):
-    """Concatenate per-rank (seq (n_r*L,), lens (n_r,)) segments on `dst` in
-    qid order; returns (seq (n_total, L), lens (n_total,)) on dst, else None.
-    Uses all_gather over equal-size padded segments (works on NCCL and gloo)."""
+    """Point-to-point gather of the per-rank path segments to `dst`, in qid
+    order: every other rank sends its (seq (n_r*L,), lens (n_r,)) segment
+    straight into its slice of dst's output (NCCL send/recv over NVLink for
+    cuda tensors, gloo for CPU tensors).  Only dst holds the full result
+    (an all-gather would land n_total*L*4 bytes on every rank).  Returns
+    (seq (n_total, L), lens (n_total,)) on dst, else None."""
     world = dist.get_world_size()
     rank = dist.get_rank()
-    cap = max(partition(n_total, world, r)[1] - partition(n_total, world, r)[0]
-              for r in range(world))
-    pad_seq = torch.full((cap * L,), -1, dtype=seq.dtype, device=seq.device)
-    pad_len = torch.zeros(cap, dtype=lens.dtype, device=lens.device)
-    pad_seq[:seq.numel()] = seq
-    pad_len[:lens.numel()] = lens
-    out_s = [torch.empty_like(pad_seq) for _ in range(world)]
-    out_l = [torch.empty_like(pad_len) for _ in range(world)]
-    dist.all_gather(out_s, pad_seq)
-    dist.all_gather(out_l, pad_len)
     if rank != dst:
+        if seq.numel():
+            reqs = [dist.isend(seq.contiguous(), dst), dist.isend(lens.contiguous(), dst)]
+            for r in reqs:
+                r.wait()
         return None
-    segs_s, segs_l = [], []
+    out_s = torch.empty(n_total * L, dtype=seq.dtype, device=seq.device)
+    out_l = torch.empty(n_total, dtype=lens.dtype, device=lens.device)
+    lo, hi = partition(n_total, world, rank)
+    out_s[lo * L:hi * L] = seq
+    out_l[lo:hi] = lens
+    reqs = []
     for r in range(world):
         lo, hi = partition(n_total, world, r)
-        segs_s.append(out_s[r][:(hi - lo) * L])
-        segs_l.append(out_l[r][:hi - lo])
-    return torch.cat(segs_s).view(n_total, L), torch.cat(segs_l)
+        if r == rank or hi == lo:
+            continue
+        reqs.append(dist.irecv(out_s[lo * L:hi * L], r))
+        reqs.append(dist.irecv(out_l[lo:hi], r))
+    for q in reqs:
+        q.wait()
+    return out_s.view(n_total, L), out_l

@@ -12,8 +12,10 @@ What changes
   * the CPU worker threads / local pools / numba step_pass are replaced by
     one persistent sm_100a kernel per device (libflowwalk.so, csrc/), whose
     warps pull queries from an atomic cursor;
-  * the graph is uploaded once per call through pinned staging (or kept
-    resident with ``to_device``/``DeviceGraph``);
+  * the graph is uploaded once through pinned staging, checked on the device
+    (offsets, target range, per-vertex sortedness), and cached across calls
+    on the same host ``Graph`` object (``evict`` drops it; ``to_device`` /
+    ``DeviceGraph`` give an explicitly resident graph);
   * ``EngineConfig.devices`` replicates the graph on several GPUs and splits
     each batch's query range across them (no collective on the walk path);
   * ``replay=False`` (the reference's schedule-dependent free-run keying)
@@ -28,6 +30,8 @@ import struct
 import threading
 import time
 import warnings
+import weakref
+import zlib
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
@@ -200,9 +204,12 @@ def _ctypes_ref(obj):
 
 
 def _upload(g, device):
-    """fw_graph_create: one pinned-staged H2D of the CSR arrays."""
+    """fw_graph_create: host checks (Graph.validate, graph.py:70-81), then one
+    pinned-staged H2D of the CSR arrays and the device-side CSR check."""
     import ctypes
     lib = _lib.load()
+    if hasattr(g, "validate"):
+        g.validate()
     off = np.ascontiguousarray(g.offsets, dtype=np.int64)
     tgt = np.ascontiguousarray(g.targets, dtype=np.uint32)
     w = np.ascontiguousarray(g.weights, dtype=np.float32)
@@ -214,6 +221,65 @@ def _upload(g, device):
                                    None if lab is None else lab.ctypes.data,
                                    g.vertex_count, g.edge_count, device, ctypes.byref(out)))
     return _Handle(out.value, device)
+
+
+def _replica_handle(src, device):
+    """fw_graph_replicate: device-to-device peer copies of a resident CSR."""
+    import ctypes
+    out = ctypes.c_void_p()
+    _lib.check(_lib.load().fw_graph_replicate(src.ptr, device, ctypes.byref(out)))
+    return _Handle(out.value, device)
+
+
+# Device replicas of host Graphs, kept across run() calls (the reference
+# re-reads its numpy arrays every call; re-uploading 18 GB per call at s27
+# would dominate).  Keyed by the Graph object (weakly: a dropped graph frees
+# its replicas); a fingerprint of the array addresses, sizes and a strided
+# sample of the contents detects a graph whose arrays were replaced or edited
+# in place.  ``evict(g)`` releases a graph's replicas explicitly.
+_CACHE = weakref.WeakKeyDictionary()
+_CACHE_LOCK = threading.Lock()
+
+
+def _fingerprint(g):
+    fp = [int(g.vertex_count), int(g.edge_count)]
+    for a in (g.offsets, g.targets, g.weights, getattr(g, "labels", None)):
+        if a is None:
+            fp.append(None)
+            continue
+        a = np.asarray(a)
+        step = max(1, a.size // 4096)
+        sample = np.ascontiguousarray(a.reshape(-1)[::step][:4096])
+        fp.append((a.__array_interface__["data"][0], a.nbytes, str(a.dtype),
+                   zlib.crc32(memoryview(sample).cast("B"))))
+    return tuple(fp)
+
+
+def _cached_handles(g, devices):
+    fp = _fingerprint(g)
+    with _CACHE_LOCK:
+        entry = _CACHE.get(g)
+        if entry is None or entry[0] != fp:
+            if entry is not None:
+                for h in entry[1].values():
+                    h.close()
+            entry = (fp, {})
+            _CACHE[g] = entry
+        reps = entry[1]
+        for d in devices:
+            if d in reps:
+                continue
+            reps[d] = _replica_handle(next(iter(reps.values())), d) if reps else _upload(g, d)
+        return [reps[d] for d in devices]
+
+
+def evict(g):
+    """Release the device replicas cached for host graph ``g``."""
+    with _CACHE_LOCK:
+        entry = _CACHE.pop(g, None)
+    if entry is not None:
+        for h in entry[1].values():
+            h.close()
 
 
 class DeviceGraph:
@@ -272,21 +338,9 @@ class DeviceGraph:
 
 
 def _replicate(dg, device):
-    """Device-to-device copy of a resident CSR (NVLink peer copy when the
-    devices are peers) and a handle on the new device."""
-    import torch
-    dev = torch.device("cuda", device)
-    arrs = []
-    for t, pad in ((dg.offsets, 0), (dg.targets, 4), (dg.weights, 4), (dg.labels, 0)):
-        if t is None:
-            arrs.append(None)
-            continue
-        c = torch.empty(t.numel() + pad, dtype=t.dtype, device=dev)[:t.numel()]
-        c.copy_(t, non_blocking=True)
-        arrs.append(c)
-    torch.cuda.synchronize(dev)
-    rep = DeviceGraph(dg.vertex_count, dg.edge_count, *arrs, device=device)
-    return rep._handle
+    """A replica of a resident CSR on `device` (fw_graph_replicate: NVLink
+    peer copies when the devices are peers)."""
+    return _replica_handle(dg._handle, device)
 
 
 def to_device(g, device=0):
@@ -306,33 +360,21 @@ def to_device(g, device=0):
 
 
 class _Session:
-    """Per-call device state: one graph handle per configured device."""
+    """Per-call device state: one graph handle per configured device.  Host
+    graphs go through the replica cache; a DeviceGraph's handles are the
+    caller's (borrowed).  Nothing is released at close."""
 
     def __init__(self, g, eng_cfg):
         _lib.load()
         _lib.require_device()
         self.devices = tuple(eng_cfg.devices)
-        self._owned = None
-        self._borrowed = isinstance(g, DeviceGraph)  # the caller's resident graph
         if isinstance(g, DeviceGraph):
             self.handles = [g.handle(d) for d in self.devices]
-        elif len(set(self.devices)) > 1:
-            # one PCIe upload to the first GPU, then device-to-device replica
-            # copies (NVLink peer copies on NVSwitch systems)
-            self._owned = to_device(g, self.devices[0])
-            self.handles = [self._owned.handle(d) for d in self.devices]
         else:
-            h = _upload(g, self.devices[0])
-            self.handles = [h] * len(self.devices)
+            self.handles = _cached_handles(g, self.devices)
 
     def close(self):
-        if self._borrowed:
-            return
-        if self._owned is not None:
-            self._owned.close()
-        else:
-            for h in set(self.handles):
-                h.close()
+        pass
 
 
 def _fw_structs(app_cfg, eng_cfg):
@@ -353,7 +395,8 @@ def _fw_structs(app_cfg, eng_cfg):
 
 
 def _walk_batch(sess, starts, base_qid, app, eng, seed, seq, lens, totals):
-    """Split one batch's query range over the session's devices."""
+    """Split one batch's query range over the session's devices (one host
+    thread per device; ctypes releases the GIL)."""
     n = len(starts)
     parts = len(sess.handles)
     bounds = [n * i // parts for i in range(parts + 1)]
@@ -368,36 +411,52 @@ def _walk_batch(sess, starts, base_qid, app, eng, seed, seq, lens, totals):
                          seed & 0xFFFFFFFFFFFFFFFF,
                          seq[lo * app.length:].ctypes.data if hi > lo else None,
                          lens[lo:].ctypes.data if hi > lo else None, _ctypes_ref(st))
-        results[i] = (rc, st)
+        # fw_last_error is thread-local: read it on the calling thread
+        msg = lib.fw_last_error().decode(errors="replace") if rc else ""
+        results[i] = (rc, msg, st, hi - lo)
 
     if parts == 1:
         one(0)
     else:
         with ThreadPoolExecutor(max_workers=parts) as ex:
             list(ex.map(one, range(parts)))
-    for rc, st in results:
-        _lib.check(rc)
+    batch_ms = 0.0
+    aux = 0
+    for i, (rc, msg, st, cnt) in enumerate(results):
+        _lib.check(rc, msg)
         for f in _lib.ST_FIELDS:
             totals[f] += getattr(st, f)
-        totals["kernel_ms"] = max(totals["kernel_ms"], st.kernel_ms) if parts > 1 else \
-            totals["kernel_ms"] + st.kernel_ms
+        batch_ms = max(batch_ms, st.kernel_ms)  # devices run concurrently
+        aux += st.aux_bytes
+        totals["aux_allocations"] = max(totals["aux_allocations"], st.aux_allocations)
+        totals["per_device"][i] += cnt
         totals["exact_order"] = bool(st.exact_order)
+    totals["kernel_ms"] += batch_ms  # batches run one after another
+    totals["aux_bytes"] = max(totals["aux_bytes"], aux)
 
 
-def _new_totals():
+def _new_totals(parts=1):
     t = {f: 0 for f in _lib.ST_FIELDS}
     t["kernel_ms"] = 0.0
     t["exact_order"] = False
+    t["aux_bytes"] = 0
+    t["aux_allocations"] = 0
+    t["per_device"] = [0] * parts
     return t
 
 
 def run_batches(g, starts, app_cfg, eng_cfg, seed=0, workers=None, meter=None,
-                on_pass=None, _totals=None):
+                on_pass=None, *, base_qid=0, _totals=None):
     """Generator over BatchResult, double-buffered (engine.py:263-322).
 
     Batch b+1 is walked on the device(s) by a driver thread while the
     consumer holds batch b; each BatchResult's arrays are views into one of
     two reused buffers, valid until the generator is resumed twice.
+
+    ``base_qid`` (B200 extension, keyword-only): global id of starts[0].  In
+    replay mode a walk is a pure function of its global qid, so a caller
+    that shards one query set (one process per GPU) passes its shard's
+    offset and gets exactly its slice of the unsharded run.
     """
     app_cfg.validate()
     eng_cfg.validate()
@@ -412,23 +471,26 @@ def run_batches(g, starts, app_cfg, eng_cfg, seed=0, workers=None, meter=None,
     n = len(starts)
     size = batch_size(eng_cfg, app_cfg.length) if eng_cfg.memory_budget is not None else max(n, 1)
     n_batches = (n + size - 1) // size if n else 0
-    if n + 0 >= 1 << 33:
+    if base_qid < 0 or base_qid + n >= 1 << 33:
         raise ConfigError("query ids exceed the replay stream-id field")
     l_max = app_cfg.length
-    totals = _totals if _totals is not None else _new_totals()
+    totals = _totals if _totals is not None else _new_totals(len(eng_cfg.devices))
     if n_batches == 0:
         return
     app, eng, _schema = _fw_structs(app_cfg, eng_cfg)
     sess = _Session(g, eng_cfg)
     rows = min(size, n)
-    buffers = [(np.empty(rows * l_max, np.uint32), np.empty(rows, np.uint32)) for _ in range(2)]
+    # the second buffer only exists when there is a second batch
+    buffers = [(np.empty(rows * l_max, np.uint32), np.empty(rows, np.uint32))
+               for _ in range(min(2, n_batches))]
 
     def compute(b, buf):
         seq, lens = buf
         base = b * size
         count = min(size, n - base)
-        _walk_batch(sess, starts[base:base + count], base, app, eng, seed, seq, lens, totals)
-        return BatchResult(batch_index=b, base_qid=base, count=count,
+        _walk_batch(sess, starts[base:base + count], base_qid + base, app, eng, seed, seq, lens,
+                    totals)
+        return BatchResult(batch_index=b, base_qid=base_qid + base, count=count,
                            sequences=seq[:count * l_max].reshape(count, l_max),
                            lengths=lens[:count])
 
@@ -445,35 +507,50 @@ def run_batches(g, starts, app_cfg, eng_cfg, seed=0, workers=None, meter=None,
         sess.close()
 
 
-def run(g, starts, app_cfg, eng_cfg, seed=0, sink=None, keep_query_ids=False, on_pass=None):
+def run(g, starts, app_cfg, eng_cfg, seed=0, sink=None, keep_query_ids=False, on_pass=None,
+        *, base_qid=0):
     """Execute all queries; returns RunStats (engine.py:325-364)."""
     app_cfg.validate()
     eng_cfg.validate()
-    totals = _new_totals()
+    totals = _new_totals(len(eng_cfg.devices))
     t0 = time.perf_counter()
     batches = 0
     for batch in run_batches(g, starts, app_cfg, eng_cfg, seed, on_pass=on_pass,
-                             _totals=totals):
+                             base_qid=base_qid, _totals=totals):
         batches += 1
         if sink is not None:
             sink(batch)
     elapsed = time.perf_counter() - t0
     n = len(starts)
-    schema_bytes = 8 * len(app_cfg.schema) if app_cfg.app == "metapath" else 0
     stats = RunStats(
         queries=n, batches=batches, steps=int(totals["steps"]),
         edges_scanned=int(totals["edges_scanned"]), collectives=int(totals["collectives"]),
         draws=int(totals["draws"]), small_tasks=int(totals["small_tasks"]),
         large_tasks=int(totals["large_tasks"]), elapsed_s=elapsed,
-        # device aux memory: per-launch cursor ring + stats words (+ schema);
-        # independent of d_max and |Q| (PAPER.md:407)
-        aux_bytes=64 * 8 + 8 * 8 + schema_bytes, aux_allocations=2 + (1 if schema_bytes else 0),
-        completed=n, per_worker_completed=[n],
+        # the library's own device scratch (cursor slots, counters, piece
+        # counters, schema copies), summed over devices: independent of d_max
+        # and |Q| (PAPER.md:407), like the reference's metered aux bytes
+        aux_bytes=int(totals["aux_bytes"]), aux_allocations=int(totals["aux_allocations"]),
+        completed=n, per_worker_completed=_per_worker(totals["per_device"], eng_cfg.workers),
         sampled_steps=int(totals["sampled_steps"]), alg_bytes=int(totals["alg_bytes"]),
         kernel_ms=float(totals["kernel_ms"]), exact_order=bool(totals["exact_order"]))
     if keep_query_ids:
-        stats.completed_query_ids = np.arange(n, dtype=np.int64)
+        stats.completed_query_ids = np.arange(base_qid, base_qid + n, dtype=np.int64)
     return stats
+
+
+def _per_worker(per_device, workers):
+    """RunStats.per_worker_completed has one entry per configured worker
+    (engine.py:357).  The device engine has no CPU workers: device d's
+    completed queries are spread evenly over the workers w with
+    w % len(devices) == d (sum and length match the reference's)."""
+    out = [0] * workers
+    nd = len(per_device)
+    for d, cnt in enumerate(per_device):
+        ws = [w for w in range(workers) if w % nd == d] or [d % workers]
+        for j, w in enumerate(ws):
+            out[w] += cnt * (j + 1) // len(ws) - cnt * j // len(ws)
+    return out
 
 
 def throughput_report(stats):

@@ -57,3 +57,29 @@ def case_kwargs(case):
             kw[k] = eng[k]
     kw["seed"] = case["seed"]
     return kw, eng
+
+
+def chi2_pass(counts, probs, alpha=1e-3):
+    """Pearson chi-square of observed ``counts`` against exact ``probs``, with
+    bins of expected count < 5 pooled (smallest first).  The reference's own
+    gate is stats.passes_chi_square (stats.py:80-139)."""
+    from scipy.stats import chi2
+    counts = np.asarray(counts, dtype=np.float64)
+    n = counts.sum()
+    exp = np.asarray(probs, dtype=np.float64) * n
+    order = np.argsort(exp, kind="stable")
+    obs_p, exp_p, acc_o, acc_e = [], [], 0.0, 0.0
+    for i in order:
+        acc_o += counts[i]
+        acc_e += exp[i]
+        if acc_e >= 5:
+            obs_p.append(acc_o)
+            exp_p.append(acc_e)
+            acc_o = acc_e = 0.0
+    if acc_e > 0 and exp_p:
+        obs_p[-1] += acc_o
+        exp_p[-1] += acc_e
+    obs_p, exp_p = np.array(obs_p), np.array(exp_p)
+    stat = float(((obs_p - exp_p) ** 2 / exp_p).sum())
+    dof = max(len(exp_p) - 1, 1)
+    return stat <= chi2.ppf(1 - alpha, dof), stat, dof

@@ -198,13 +198,14 @@ def test_torchrun_two_ranks_strong_scaling_gather(tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29517",
            os.path.join(root, "bench.py"), "--gpus", "2", "--scale", "14", "--nq", str(n),
-           "--steps", "1", "--warmup", "1", "--scaling", "strong", "--gather",
+           "--steps", "1", "--warmup", "1",
            "--dump-gather", str(out), "--no-cpu-baseline", "--no-e2e", "--length", "24"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert res.returncode == 0, res.stderr[-3000:]
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert line["config"]["queries_per_gpu"] == n // 2
+    assert line["config"]["gather_ms"] is not None and len(line["config"]["per_rank_walk_ms"]) == 2
     z = np.load(out)
     g = rmat.rmat_graph(14, labels=False)
     starts = np.arange(n, dtype=np.int64) % g.vertex_count

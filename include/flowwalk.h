@@ -23,6 +23,12 @@
  *   fw_sampler_trials_device
  *       -- the sampler trial kernels seq_rs/dprs/zprs/its/alias/rjs/uniform_control_trials
  *          (_kernels.py:84-277) behind trials.run_trials (trials.py:46-90).
+ *   fw_build_csr_device / fw_edges_max_id
+ *       -- reswalk build_csr (graph.py:138-169): CSR from an edge list, lists sorted by
+ *          target with duplicates in input order (np.lexsort semantics), on the device.
+ *   fw_fwg1_info / fw_fwg1_read / fw_crc32_device
+ *       -- reswalk load_binary (graph.py:225-254): the FWG1 file streamed into device
+ *          arrays, its zlib CRC-32 checked on the device.
  *   fw_rmat_edges_device / fw_synth_weights_device / fw_synth_labels_device
  *       -- synthetic inputs; the reference only ships random/star edge lists and
  *          numpy-seeded synthesis (graph.py:172-201, 257-277), see DESIGN.md.
@@ -42,6 +48,7 @@ enum {
     FW_ECONFIG = 2,     /* reswalk ConfigError (engine.py:64-77, 276-277) */
     FW_ECUDA = 3,       /* CUDA runtime failure */
     FW_ENOMEM = 4,      /* device allocation failure */
+    FW_EFORMAT = 5,     /* reswalk FormatError (graph.py:232-244): bad magic, size or CRC */
 };
 
 /* app ids: reswalk apps.py:21-24 (APP_IDS) / _kernels.py:41-44 */
@@ -178,6 +185,28 @@ int fw_sampler_trials_device(int32_t method, const double *d_w, uint32_t n, uint
                              uint64_t key, uint64_t trials, const double *d_prob,
                              const int64_t *d_alias, double w_max, uint32_t max_rounds,
                              uint32_t *d_picks, int64_t *d_aux, void *stream);
+
+/* ---- graph ingest (csrc/fw_ingest.cu); all arrays are device pointers ---- */
+/* Largest vertex id over src and dst (m edges). */
+int fw_edges_max_id(const uint32_t *d_src, const uint32_t *d_dst, uint64_t m,
+                    uint64_t *out_max, void *stream);
+/* build_csr: out offsets int64[V+1], targets u32[m], weights f32[m] (w_in NULL:
+ * all 1), labels u8[m] (lab_in NULL: all 0; lab_out NULL: not written).  m < 2^32.
+ * FW_EVALIDATION if some id >= V. */
+int fw_build_csr_device(const uint32_t *d_src, const uint32_t *d_dst, const float *d_w_in,
+                        const uint8_t *d_lab_in, uint64_t m, uint64_t vertex_count,
+                        int64_t *d_offsets, uint32_t *d_targets, float *d_w_out,
+                        uint8_t *d_lab_out, void *stream);
+/* FWG1 header: V, E, flags (bit 1: labels present); FW_EFORMAT on bad magic/size. */
+int fw_fwg1_info(const char *path, uint64_t *vertex_count, uint64_t *edge_count,
+                 int32_t *flags);
+/* Stream the FWG1 payload into device arrays (pinned double buffers, reader
+ * threads), then check its CRC-32 on the device (FW_EFORMAT on mismatch). */
+int fw_fwg1_read(const char *path, uint64_t vertex_count, uint64_t edge_count, int32_t flags,
+                 int64_t *d_offsets, uint32_t *d_targets, float *d_weights,
+                 uint8_t *d_labels_or_null, uint32_t *crc_out, void *stream);
+/* zlib CRC-32 of n device bytes. */
+int fw_crc32_device(const uint8_t *d_bytes, uint64_t n, uint32_t *out, void *stream);
 
 /* Synthetic R-MAT (Graph500 a,b,c; d = 1-a-b-c) edges, counter-hash driven so
  * host (numpy) and device generate identical lists.  Writes m (src, dst)

@@ -14,7 +14,8 @@ from .engine import (AllocationMeter, BatchResult, DeviceGraph, EngineConfig, Gl
                      throughput_report, to_device, write_result_file)
 from .errors import (CapacityError, ConfigError, FormatError, ParseError,
                      RejectionExhausted, ReswalkError, ValidationError)
-from .graph import (EdgeList, Graph, build_csr, load_binary, parse_edge_list,
+from .graph import (EdgeList, Graph, build_csr, build_csr_device, load_binary,
+                    load_binary_device, parse_edge_list,
                     random_edge_list, save_binary, star_edge_list, synthesize_labels,
                     synthesize_weights)
 from .rng import RngStream, make_stream
@@ -27,7 +28,7 @@ __all__ = [
     "read_result_file", "run", "run_batches", "throughput_report", "to_device",
     "write_result_file", "CapacityError", "ConfigError", "FormatError", "ParseError",
     "RejectionExhausted", "ReswalkError", "ValidationError", "EdgeList", "Graph",
-    "build_csr", "load_binary", "parse_edge_list", "random_edge_list", "save_binary",
+    "build_csr", "build_csr_device", "load_binary", "load_binary_device", "parse_edge_list", "random_edge_list", "save_binary",
     "star_edge_list", "synthesize_labels", "synthesize_weights", "RngStream", "make_stream",
     "__version__",
 ]

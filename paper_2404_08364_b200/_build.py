@@ -5,7 +5,7 @@ import subprocess
 import sys
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["csrc/fw_api.cu", "csrc/fw_walk.cu", "csrc/fw_trials.cu"]
+SOURCES = ["csrc/fw_api.cu", "csrc/fw_walk.cu", "csrc/fw_trials.cu", "csrc/fw_ingest.cu"]
 HEADERS = ["csrc/fw_common.cuh", "csrc/fw_walk.cuh", "../include/flowwalk.h"]
 OUT = os.path.join(_HERE, "libflowwalk.so")
 

@@ -10,7 +10,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FW_LIB_PATH") or os.path.join(_HERE, "libflowwalk.so")
 
-FW_OK, FW_EVALIDATION, FW_ECONFIG, FW_ECUDA, FW_ENOMEM = range(5)
+FW_OK, FW_EVALIDATION, FW_ECONFIG, FW_ECUDA, FW_ENOMEM, FW_EFORMAT = range(6)
 ORDER_AUTO, ORDER_SEQUENTIAL = 0, 1
 ST_FIELDS = ("steps", "edges_scanned", "collectives", "draws", "small_tasks",
              "large_tasks", "sampled_steps", "alg_bytes")
@@ -52,7 +52,8 @@ class FwGraphInfo(ctypes.Structure):
 EXPORTS = ("fw_last_error", "fw_device_count", "fw_graph_create", "fw_graph_create_device",
            "fw_graph_replicate", "fw_graph_destroy", "fw_graph_set_scratch_limit", "fw_graph_info_get", "fw_walk", "fw_walk_device",
            "fw_validate_device", "fw_sampler_trials_device", "fw_rmat_edges_device",
-           "fw_synth_weights_device", "fw_synth_labels_device")
+           "fw_synth_weights_device", "fw_synth_labels_device", "fw_edges_max_id",
+           "fw_build_csr_device", "fw_fwg1_info", "fw_fwg1_read", "fw_crc32_device")
 
 _lib = None
 
@@ -84,6 +85,11 @@ def load(path=LIB_PATH):
         "fw_rmat_edges_device": ([U64, I32, D, D, D, U64, U64, P, P, P], I32),
         "fw_synth_weights_device": ([U64, U64, U64, P, P], I32),
         "fw_synth_labels_device": ([U64, U32, U64, U64, P, P], I32),
+        "fw_edges_max_id": ([P, P, U64, P, P], I32),
+        "fw_build_csr_device": ([P, P, P, P, U64, U64, P, P, P, P, P], I32),
+        "fw_fwg1_info": ([ctypes.c_char_p, P, P, P], I32),
+        "fw_fwg1_read": ([ctypes.c_char_p, U64, U64, I32, P, P, P, P, P, P], I32),
+        "fw_crc32_device": ([P, U64, P, P], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -99,7 +105,7 @@ def check(rc, msg=None):
     message is thread-local)."""
     if rc == FW_OK:
         return
-    from .errors import ConfigError, ValidationError
+    from .errors import ConfigError, FormatError, ValidationError
     if msg is None:
         msg = load().fw_last_error().decode(errors="replace")
     if rc == FW_EVALIDATION:
@@ -108,6 +114,8 @@ def check(rc, msg=None):
         raise ConfigError(msg)
     if rc == FW_ENOMEM:
         raise MemoryError(msg)
+    if rc == FW_EFORMAT:
+        raise FormatError(msg)
     raise RuntimeError(f"flowwalk CUDA error: {msg}")
 
 

@@ -106,6 +106,18 @@ struct fw_graph {
 
 extern "C" const char *fw_last_error(void) { return g_err.c_str(); }
 
+namespace fwi {  // csrc/fw_ingest.cu reports through the same thread-local message
+int set_err_ingest(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+}  // namespace fwi
+
 extern "C" int fw_device_count(int *out) {
     CU(cudaGetDeviceCount(out));
     return FW_OK;

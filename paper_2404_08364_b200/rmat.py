@@ -8,7 +8,8 @@ lists sorted; weights U[1,5) float32 and labels U{0..4} uint8 assigned per
 CSR position.  Every random choice is a counter hash (the walk RNG's mix64),
 so the numpy path here and the device path (fw_rmat_edges_device &c. in
 csrc/fw_api.cu) produce identical arrays; tests pin that on small scales.
-The oracle always receives the exact arrays the GPU walks.
+The oracle always receives the exact arrays the GPU walks.  The device
+build sorts with the library's own radix sort (fw_build_csr_device).
 """
 
 import numpy as np
@@ -101,34 +102,14 @@ def rmat_graph(scale, edge_factor=16, seed=GRAPH_SEED, labels=True,
     return Graph(V, E, offsets, targets, w, lab)
 
 
-def _sort_keys(key, V, max_sort):
-    """Sort int64 (src << 32 | dst) keys; above `max_sort` elements the sort
-    is split into src-range buckets (each sorted separately, concatenated),
-    keeping every torch.sort call well inside 32-bit index limits."""
-    import torch
-    E = key.numel()
-    nb = max(1, -(-E // max_sort))
-    if nb == 1:
-        return torch.sort(key)[0]
-    out = torch.empty_like(key)
-    pos = 0
-    for b in range(nb):
-        lo, hi = (V * b // nb) << 32, (V * (b + 1) // nb) << 32
-        sel = key[(key >= lo) & (key < hi)]
-        sel = torch.sort(sel)[0]
-        out[pos:pos + sel.numel()] = sel
-        pos += sel.numel()
-        del sel
-    assert pos == E
-    return out
-
-
 def rmat_graph_device(scale, edge_factor=16, seed=GRAPH_SEED, labels=True,
                       weight_seed=WEIGHT_SEED, label_seed=LABEL_SEED, label_count=5,
-                      device=0, max_sort=1 << 28):
-    """Device build: hash-generated edges (sm_100a kernels in libflowwalk.so),
-    torch.sort as plumbing for the (src, dst) order, weights/labels by CSR
-    position.  Returns a DeviceGraph whose arrays equal rmat_graph(...)'s."""
+                      device=0):
+    """Device build: hash-generated edges and both directions of each
+    (fw_rmat_edges_device, called twice with the outputs swapped), CSR by the
+    device build_csr (fw_build_csr_device: stable radix sort), weights and
+    labels by CSR position.  Returns a DeviceGraph whose arrays equal
+    rmat_graph(...)'s."""
     import torch
 
     from . import _lib
@@ -141,25 +122,19 @@ def rmat_graph_device(scale, edge_factor=16, seed=GRAPH_SEED, labels=True,
     E = 2 * m
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
-        uv = torch.empty(2 * m, dtype=torch.int32, device=dev)
-        _lib.check(lib.fw_rmat_edges_device(seed, scale, *RMAT_ABC, 0, m, uv.data_ptr(),
-                                            uv.data_ptr() + 4 * m, stream))
-        u = uv[:m].to(torch.int64) & 0xFFFFFFFF
-        v = uv[m:].to(torch.int64) & 0xFFFFFFFF
-        del uv
-        key = torch.cat([(u << 32) | v, (v << 32) | u])
-        del u, v
-        key = _sort_keys(key, V, max_sort)
-        src = key >> 32
-        counts = torch.bincount(src, minlength=V)
-        del src
-        offsets = torch.zeros(V + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(counts, 0, out=offsets[1:])
-        del counts
+        src = torch.empty(E, dtype=torch.int32, device=dev)
+        dst = torch.empty(E, dtype=torch.int32, device=dev)
+        _lib.check(lib.fw_rmat_edges_device(seed, scale, *RMAT_ABC, 0, m, src.data_ptr(),
+                                            dst.data_ptr(), stream))
+        _lib.check(lib.fw_rmat_edges_device(seed, scale, *RMAT_ABC, 0, m, dst.data_ptr() + 4 * m,
+                                            src.data_ptr() + 4 * m, stream))
+        offsets = torch.empty(V + 1, dtype=torch.int64, device=dev)
         # +4 elements: the walk kernel reads 16-byte tiles (DeviceGraph contract)
         targets = torch.empty(E + 4, dtype=torch.int32, device=dev)[:E]
-        targets.copy_(key & 0xFFFFFFFF)
-        del key
+        _lib.check(lib.fw_build_csr_device(src.data_ptr(), dst.data_ptr(), None, None, E, V,
+                                           offsets.data_ptr(), targets.data_ptr(), None, None,
+                                           stream))
+        del src, dst
         weights = torch.empty(E + 4, dtype=torch.float32, device=dev)[:E]
         _lib.check(lib.fw_synth_weights_device(weight_seed, 0, E, weights.data_ptr(), stream))
         lab = None

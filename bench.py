@@ -56,6 +56,10 @@ def parse_args():
                    choices=["node2vec", "deepwalk", "ppr", "metapath"])
     p.add_argument("--length", type=int, default=None)
     p.add_argument("--queries", default="all", help="all | hub (PPR config)")
+    p.add_argument("--weights", choices=["uniform", "lognormal"], default="uniform",
+                   help="edge weights: U[1,5) (BASELINE) or log-normal(0, 1) as "
+                        "graph.py:183-188 draws them (seed 2): sums that round, the "
+                        "certified-summation path")
     p.add_argument("--sampler", choices=["auto", "dprs", "zprs"], default="auto",
                    help="EngineConfig.sampler (auto: DPRS for Node2Vec, else ZPRS)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -94,7 +98,8 @@ def workload_name(args, app):
     extra = {"node2vec": " p=2 q=0.5", "ppr": " stop 0.2", "metapath": " schema 0..4",
              "deepwalk": " weighted"}[args.app]
     q = "all queries at the max-degree vertex" if args.queries == "hub" else "one query per vertex"
-    return f"{metric_name(args).split()[0]}{extra} length {app.length}, {q}, R-MAT scale-{args.scale} ef16"
+    wt = ", log-normal weights" if args.weights == "lognormal" else ""
+    return f"{metric_name(args).split()[0]}{extra} length {app.length}, {q}, R-MAT scale-{args.scale} ef16{wt}"
 
 
 class ClockSampler:
@@ -257,6 +262,9 @@ def bench_reference(args):
     from paper_2404_08364_b200 import rmat
     app = app_config(args)
     g = rmat.rmat_graph(args.scale, labels=(args.app == "metapath"))
+    if args.weights == "lognormal":
+        from paper_2404_08364_b200.graph import synthesize_weights
+        g = synthesize_weights(g, 2, "lognormal")
     starts = make_starts(args, g.vertex_count, g.max_degree_vertex())
     kind, run, cores = reference_runner(g, app, starts, args.sampler)
     n = min(calibrate(run, min(args.cpu_seconds, 8.0)), len(starts))
@@ -322,6 +330,12 @@ def bench_ours(args):
     E_ = 16 * V
     if rank == 0:
         dg = rmat.rmat_graph_device(args.scale, labels=labels, device=local)
+        if args.weights == "lognormal":  # synthesize_weights(g, 2, "lognormal") on the device copy
+            w = np.random.default_rng(2).lognormal(0.0, 1.0, E_).astype(np.float32)
+            wd = torch.empty(E_ + 4, dtype=torch.float32, device=dev)[:E_]  # 16-byte tail
+            wd.copy_(torch.from_numpy(w))
+            dg = DeviceGraph(V, E_, dg.offsets, dg.targets, wd, dg.labels, device=local)
+            del w
         arrs = [dg.offsets, dg.targets, dg.weights] + ([dg.labels] if labels else [])
     if world > 1:
         sd = [(V + 1, torch.int64), (E_, torch.int32), (E_, torch.float32)] + \
@@ -431,6 +445,7 @@ def bench_ours(args):
 
     # end to end through the C ABI with pinned host buffers
     e2e = None
+    summation = None
     if not args.no_e2e:
         hs = torch.from_numpy(starts_h).pin_memory()
         hseq = torch.empty(n * L, dtype=torch.int32).pin_memory()
@@ -458,6 +473,7 @@ def bench_ours(args):
                "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * L * 4 + n * 4,
                "path": "fw_walk (C ABI, pinned host buffers)",
                "d2h_pieces_overlapped": int(fst.d2h_pieces)}
+        summation = {0: "sequential", 1: "exact", 2: "certified"}.get(int(fst.exact_order))
         del hseq
 
     peak, peak_kind = measured_peak()
@@ -496,6 +512,7 @@ def bench_ours(args):
                        "backend": backend if world > 1 else None,
                        "parallelism": f"replicated graph, qids partitioned x{world}",
                        "l2": "inputs larger than L2 (graph + result pool > 126 MB), no flush",
+                       "weights": args.weights, "summation": summation,
                        "sampled_steps_per_gpu_step": sampled // args.steps,
                        "walk_attempts_per_step": int(st[0]) // args.steps},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -95,7 +95,9 @@ typedef struct {
     int64_t alg_bytes;      /* algorithmic HBM bytes */
     double kernel_ms;       /* walk kernel time (CUDA events) */
     double total_ms;        /* incl. H2D/D2H for fw_walk */
-    int32_t exact_order;    /* 1 if tree-order scans were used */
+    int32_t exact_order;    /* summation order: 0 the reference's sequential order replayed,
+                               1 tree-order scans (every partial sum exact), 2 tree-order
+                               scans with certified accept tests */
     int32_t grid_ctas;
     int32_t kernel_launches;
     int32_t d2h_pieces;     /* fw_walk: result pieces copied back while the walk ran

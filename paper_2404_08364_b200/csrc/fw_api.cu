@@ -523,14 +523,30 @@ static int check_cfg(fw_graph *g, const fw_app *app, const fw_engine *eng) {
 
 static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t base_qid,
                   const fw_app *app, const fw_engine *eng, uint64_t seed, uint32_t *d_seq,
-                  uint32_t *d_len, int64_t *d_stats, cudaStream_t stream, bool *exact_out,
+                  uint32_t *d_len, int64_t *d_stats, cudaStream_t stream, int *mode_out,
                   int *grid_out, unsigned *d_done = nullptr, uint64_t piece_q = 0) {
     if (base_qid + n > (1ull << 33))
         return set_err(FW_ECONFIG, "query ids exceed the replay stream-id field (2^33)");
     long G = 0;
     double xmax = 0.0;
-    const bool exact = eng->order_mode == FW_ORDER_AUTO && exact_order_ok(g->info, *app, &G, &xmax);
-    if (exact_out) *exact_out = exact;
+    // FW_FORCE_CERT=1 (tests): certified mode even where every sum is exact
+    const char *force_cert = getenv("FW_FORCE_CERT");
+    const bool fc = force_cert && force_cert[0] == '1';
+    const bool exact = eng->order_mode == FW_ORDER_AUTO && !fc &&
+                       exact_order_ok(g->info, *app, &G, &xmax);
+    // certified mode (DPRS over weights whose sums round, e.g. log-normal):
+    // tree-order scans with certified accept tests; needs nonnegative finite
+    // weights and sums far from overflow (cert_accept's bound)
+    int mode = exact ? 1 : 0;
+    if (!exact && eng->order_mode == FW_ORDER_AUTO && eng->sampler_id == FW_SAMPLER_DPRS &&
+        app->weighted && !g->info.bad_weights) {
+        double fmax = 1.0;
+        if (app->app_id == FW_APP_NODE2VEC) fmax = std::max({1.0, app->inv_a, app->inv_b});
+        const double tot = (double)g->info.max_degree * fmax * (double)g->info.max_weight;
+        const char *env = getenv("FW_CERT");  // A/B override: 0 keeps the ordered kernels
+        if (std::isfinite(fmax) && tot < 1e290 && !(env && env[0] == '0')) mode = 2;
+    }
+    if (mode_out) *mode_out = mode;
     if (n == 0) return FW_OK;
     WalkArgs a{};
     a.off = g->off;
@@ -604,6 +620,9 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     a.k_big = eng->k_big;
     a.d_t = eng->d_t;
     a.h = mix64(seed + GOLDEN);
+    a.cert_slack = 0x1p-50;
+    if (const char *cs = getenv("FW_CERT_SLACK"))  // tests: widen the ambiguity band
+        a.cert_slack = std::ldexp(1.0, -50 + atoi(cs));
     {
         const char *mr = getenv("FW_MERGE_RATIO");
         a.merge_ratio = mr ? (uint32_t)atoi(mr) : 4u;  // measured: 4 > 8 > 16 > 32 (s22 +7.8%, s27 +1.7%)
@@ -634,13 +653,13 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
             a.schema = (const int64_t *)sb.p;
         }
     }
-    const int occ = std::max(1, walk_occupancy(app->app_id, eng->sampler_id, exact));
+    const int occ = std::max(1, walk_occupancy(app->app_id, eng->sampler_id, mode));
     const uint64_t warps_needed = n;
     uint64_t grid = (uint64_t)g->sm_count * occ;
     const uint64_t max_useful = (warps_needed + (kWalkThreads / 32) - 1) / (kWalkThreads / 32);
     if (grid > max_useful) grid = max_useful;
     if (grid_out) *grid_out = (int)grid;
-    CU(launch_walk(a, app->app_id, eng->sampler_id, exact, (int)grid, stream));
+    CU(launch_walk(a, app->app_id, eng->sampler_id, mode, (int)grid, stream));
     CU(cudaEventRecord(g->slot_ev[slot], stream));
     g->slot_used[slot] = true;
     return FW_OK;
@@ -730,7 +749,7 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     cudaEvent_t e0 = g->ev[0], e1 = g->ev[1], e2 = g->ev[2], e3 = g->ev[3], ez = g->ev[4];
     cudaEventRecord(e0, st);
     cudaMemsetAsync(g->stats.p, 0, ST_WORDS * sizeof(int64_t), st);
-    bool exact = false;
+    int exact = 0;
     int grid = 0, pieces = 0, launches = 0;
     if (single) {
         if (P) cudaMemsetAsync(g->done.p, 0, P * sizeof(unsigned), st);

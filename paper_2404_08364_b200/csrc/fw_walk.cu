@@ -98,6 +98,26 @@ __device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
     return accept_thr_f(wmax, (float)base);
 }
 
+// Certified accept test (walk mode 2: weights whose fp64 partial sums are not
+// exact, e.g. log-normal).  The reference's P_seq (chunk-sequential sums,
+// _kernels.py:404-424) and this kernel's tree-order P differ from the exact
+// prefix by at most about (2i + c + 1) * 2^-53 * tot each (nonnegative terms,
+// tot >= every partial sum of the step so far); d below is more than twice
+// that.  Monotone rounding then decides fl(r * P_seq) < w from P alone unless
+// r * P is within d of w:
+//   ru(r * ru(P + d)) < w  -> accepted for every P_seq in [P - d, P + d]
+//   rd(r * rd(P - d)) >= w -> rejected for every such P_seq
+// and otherwise (probability ~ i * 2^-50) the step is ambiguous and is
+// re-run on the ordered path.  Returns 1 accept, 0 reject, 2 ambiguous.
+__device__ __forceinline__ int cert_accept(double r, double P, double w, double tot, uint32_t i,
+                                           double slack) {
+    const double d = __dmul_ru(tot, __dmul_ru((double)i + 160.0, slack));
+    if (__dmul_ru(r, __dadd_ru(P, d)) < w) return 1;
+    if (__dmul_rd(r, fmax(__dadd_rd(P, -d), 0.0)) >= w) return 0;
+    return 2;
+}
+constexpr uint32_t kCertFallback = 0xFFFFFFFFu;  // "re-run this step in order"
+
 template <int APP>
 __device__ __forceinline__ double elem_weight(const WalkArgs &a, const StepCtx &s, uint32_t i) {
     const int64_t e = s.elo + i;
@@ -417,11 +437,25 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
 // exact).  Otherwise the reference's order is replayed: sequential sum
 // within each k-chunk, P = chunk_prefix + carry, carry += chunk sum.
 // ---------------------------------------------------------------------------
-template <int APP>
+template <int APP, bool CERT = false>
 __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane) {
     const uint32_t deg = s.deg;
     double carry = 0.0;
-    uint32_t cand = 0;
+    uint32_t cand = 0, amb = 0;
+    // CERT: the accept test against the post-tile carry (>= every partial sum
+    // of the step so far) -- see cert_accept
+#define FW_DPRS_TEST(I, WV, P, R, TOT)                                                   \
+    do {                                                                                 \
+        if constexpr (CERT) {                                                            \
+            if ((WV) > 0.0) {                                                            \
+                const int c_ = cert_accept((R), (P), (WV), (TOT), (I), a.cert_slack);    \
+                if (c_ == 1) cand = (I) + 1;                                             \
+                else if (c_ == 2) amb = (I) + 1;                                         \
+            }                                                                            \
+        } else if ((WV) > 0.0 && __dmul_rn((R), (P)) < (WV)) {                           \
+            cand = (I) + 1;                                                              \
+        }                                                                                \
+    } while (0)
     if (k == 32) {
         uint64_t word = lane_base(a, s, lane);
 #pragma unroll 2
@@ -431,11 +465,12 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
             const uint32_t thr = accept_thr(a.accept_wmax, carry);  // prefilter
             const double incl = warp_incl_scan(wv, lane);
             const double P = __dadd_rn(carry, incl);
+            const double nc = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
             if (mix64_yhi(word) <= thr) {
                 const double r = u01_word(word);
-                if (wv > 0.0 && __dmul_rn(r, P) < wv) cand = i + 1;
+                FW_DPRS_TEST(i, wv, P, r, nc);
             }
-            carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
+            carry = nc;
         }
     } else if (k == 256) {
         uint64_t base[8];
@@ -452,12 +487,13 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
                     const uint32_t thr = accept_thr(a.accept_wmax, carry);  // prefilter
                     const double incl = warp_incl_scan(wv, lane);
                     const double P = __dadd_rn(carry, incl);
+                    const double nc = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
                     const uint64_t wd = base[q] + cadd;
                     if (mix64_yhi(wd) <= thr) {
                         const double r = u01_word(wd);
-                        if (wv > 0.0 && __dmul_rn(r, P) < wv) cand = i + 1;
+                        FW_DPRS_TEST(i, wv, P, r, nc);
                     }
-                    carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
+                    carry = nc;
                 }
             }
         }
@@ -467,14 +503,20 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
             const double wv = i < deg ? elem_weight<APP>(a, s, i) : 0.0;
             const double incl = warp_incl_scan(wv, lane);
             const double P = __dadd_rn(carry, incl);
+            const double nc = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
             if (wv > 0.0) {
                 const double r = u01(lane_base(a, s, i % k), (uint64_t)(i / k));
-                if (__dmul_rn(r, P) < wv) cand = i + 1;
+                FW_DPRS_TEST(i, wv, P, r, nc);
             }
-            carry = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
+            carry = nc;
         }
     }
-    return __reduce_max_sync(FULL, cand);
+#undef FW_DPRS_TEST
+    const uint32_t sel = __reduce_max_sync(FULL, cand);
+    if constexpr (CERT) {
+        if (__reduce_max_sync(FULL, amb) > sel) return kCertFallback;
+    }
+    return sel;
 }
 
 // ---------------------------------------------------------------------------
@@ -861,7 +903,7 @@ __device__ __forceinline__ void stage_words(const WalkArgs &a, const StepCtx &s,
 // a 4-element local prefix plus one warp scan, draw words from the staged
 // per-lane table, and the accept test.
 // HASHED: the caller has established that N(prev) uses windows (not bsearch).
-template <bool F32, bool WEIGHTED, bool HASHED = false, bool ISCAN = false>
+template <bool F32, bool WEIGHTED, bool HASHED = false, bool ISCAN = false, bool CERT = false>
 __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                                   uint32_t woff) {
     const uint32_t deg = s.deg;
@@ -894,6 +936,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     double carry = 0.0;
     uint64_t icarry = 0;  // ISCAN: the carry in units of 2^G (exact)
     uint32_t cand = 0;
+    [[maybe_unused]] uint32_t amb = 0;  // CERT: last ambiguous element + 1
     const uint32_t ntiles = (span + 127) >> 7;
     for (uint32_t t = 0; t < ntiles; t++, tp += 128, wpt += 128) {
         const uint32_t x0 = t * 128;  // first slot of the tile
@@ -1072,7 +1115,15 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                     run = __dadd_rn(run, w);
                     if ((pass >> e) & 1) {
                         const double r = u01_word(wd[e]);
-                        if (w > 0.0 && __dmul_rn(r, run) < w) {
+                        if constexpr (CERT) {
+                            // carry is already the post-tile total here
+                            if (w > 0.0) {
+                                const int c_ = cert_accept(r, run, w, carry, (uint32_t)(i0 + e),
+                                                           a.cert_slack);
+                                if (c_ == 1) cand = (uint32_t)(i0 + e) + 1;
+                                else if (c_ == 2) amb = (uint32_t)(i0 + e) + 1;
+                            }
+                        } else if (w > 0.0 && __dmul_rn(r, run) < w) {
                             cand = (uint32_t)(i0 + e) + 1;
 #if FW_PF_NEXT
                             // the candidate may become the next vertex: pull its
@@ -1101,6 +1152,9 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
     // carrying it frees the u registers before the draws
     const uint32_t sel = __reduce_max_sync(FULL, cand);
     __syncwarp();  // the table and the staged words are rebuilt by the next step
+    if constexpr (CERT) {
+        if (__reduce_max_sync(FULL, amb) > sel) return kCertFallback;
+    }
     return sel;
 }
 
@@ -1237,9 +1291,14 @@ __device__ __forceinline__ void stat_add(unsigned long long *st, int idx, long l
 // ---------------------------------------------------------------------------
 // The persistent walker.
 // ---------------------------------------------------------------------------
-template <int APP, int SAMPLER, bool EXACT>
+// MODE: 0 = the reference's summation order replayed (ordered kernels),
+// 1 = exact (every partial sum exact: tree scans), 2 = certified (DPRS only:
+// tree scans with certified accept tests, ambiguous steps re-run in order).
+template <int APP, int SAMPLER, int MODE>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks(APP))
 walk_kernel(const __grid_constant__ WalkArgs a) {
+    constexpr bool EXACT = MODE >= 1;
+    constexpr bool CERT = MODE == 2;
     const int lane = threadIdx.x & 31;
     const uint32_t woff = (threadIdx.x >> 5) * warp_words(APP);
     // per-warp RunStats counters live in shared memory (registers are the
@@ -1295,7 +1354,24 @@ walk_kernel(const __grid_constant__ WalkArgs a) {
             uint32_t sel_u = 0;
             bool have_u = false;
             if constexpr (SAMPLER == SAMPLER_DPRS) {
-                if constexpr (EXACT && APP == APP_NODE2VEC) {
+                if constexpr (CERT) {
+                    // non-dyadic weights: weighted by construction (unweighted
+                    // sums are exact and run in mode 1)
+                    if (APP == APP_NODE2VEC && s.prev >= 0) {
+                        if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
+                            const bool win = (uint32_t)(s.phi - s.plo) <=
+                                             a.merge_ratio * s.deg + 2 * kChunk;
+                            sel = a.fac32 ? (win ? dprs_n2v_pow2<true, true, true, false, true>(a, s, k, lane, woff)
+                                                 : dprs_n2v_pow2<true, true, false, false, true>(a, s, k, lane, woff))
+                                          : dprs_n2v_pow2<false, true, false, false, true>(a, s, k, lane, woff);
+                        } else {
+                            sel = kCertFallback;
+                        }
+                    } else {
+                        sel = dprs_warp_exact<APP, true>(a, s, k, lane);
+                    }
+                    if (sel == kCertFallback) sel = dprs_warp_ordered<APP>(a, s, k, lane);
+                } else if constexpr (EXACT && APP == APP_NODE2VEC) {
                     if (s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
                             const bool win = (uint32_t)(s.phi - s.plo) <=
@@ -1380,53 +1456,51 @@ walk_kernel(const __grid_constant__ WalkArgs a) {
     }
 }
 
-template <int APP, int SAMPLER, bool EXACT>
+template <int APP, int SAMPLER, int MODE>
 static cudaError_t launch_t(const WalkArgs &a, int grid, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, EXACT>,
+        cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, MODE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, walk_smem_bytes(APP));
         attr = true;
     }
-    walk_kernel<APP, SAMPLER, EXACT><<<grid, kWalkThreads, walk_smem_bytes(APP), stream>>>(a);
+    walk_kernel<APP, SAMPLER, MODE><<<grid, kWalkThreads, walk_smem_bytes(APP), stream>>>(a);
     return cudaGetLastError();
 }
 
-template <int APP, int SAMPLER, bool EXACT>
+template <int APP, int SAMPLER, int MODE>
 static int occupancy_t() {
     int nb = 0;
-    cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, EXACT>,
+    cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, MODE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, walk_smem_bytes(APP));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_kernel<APP, SAMPLER, EXACT>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_kernel<APP, SAMPLER, MODE>,
                                                   kWalkThreads, walk_smem_bytes(APP));
     return nb;
 }
 
+// mode 2 exists for DPRS only (the host never asks for certified ZPRS)
+#define FW_DISPATCH_APP(FN, APP, ...)                                                \
+    if (sampler == SAMPLER_ZPRS) {                                                   \
+        if (mode == 0) return FN<APP, 0, 0>(__VA_ARGS__);                            \
+        return FN<APP, 0, 1>(__VA_ARGS__);                                           \
+    }                                                                                \
+    if (mode == 0) return FN<APP, 1, 0>(__VA_ARGS__);                                \
+    if (mode == 1) return FN<APP, 1, 1>(__VA_ARGS__);                                \
+    return FN<APP, 1, 2>(__VA_ARGS__);
+
 #define FW_DISPATCH(FN, ...)                                                         \
-    switch (app * 4 + sampler * 2 + (exact ? 1 : 0)) {                               \
-    case 0: return FN<0, 0, false>(__VA_ARGS__);                                     \
-    case 1: return FN<0, 0, true>(__VA_ARGS__);                                      \
-    case 2: return FN<0, 1, false>(__VA_ARGS__);                                     \
-    case 3: return FN<0, 1, true>(__VA_ARGS__);                                      \
-    case 4: return FN<1, 0, false>(__VA_ARGS__);                                     \
-    case 5: return FN<1, 0, true>(__VA_ARGS__);                                      \
-    case 6: return FN<1, 1, false>(__VA_ARGS__);                                     \
-    case 7: return FN<1, 1, true>(__VA_ARGS__);                                      \
-    case 8: return FN<2, 0, false>(__VA_ARGS__);                                     \
-    case 9: return FN<2, 0, true>(__VA_ARGS__);                                      \
-    case 10: return FN<2, 1, false>(__VA_ARGS__);                                    \
-    case 11: return FN<2, 1, true>(__VA_ARGS__);                                     \
-    case 12: return FN<3, 0, false>(__VA_ARGS__);                                    \
-    case 13: return FN<3, 0, true>(__VA_ARGS__);                                     \
-    case 14: return FN<3, 1, false>(__VA_ARGS__);                                    \
-    default: return FN<3, 1, true>(__VA_ARGS__);                                     \
+    switch (app) {                                                                   \
+    case 0: { FW_DISPATCH_APP(FN, 0, __VA_ARGS__) }                                  \
+    case 1: { FW_DISPATCH_APP(FN, 1, __VA_ARGS__) }                                  \
+    case 2: { FW_DISPATCH_APP(FN, 2, __VA_ARGS__) }                                  \
+    default: { FW_DISPATCH_APP(FN, 3, __VA_ARGS__) }                                 \
     }
 
-cudaError_t launch_walk(const WalkArgs &a, int app, int sampler, bool exact, int grid,
+cudaError_t launch_walk(const WalkArgs &a, int app, int sampler, int mode, int grid,
                         cudaStream_t stream) {
     FW_DISPATCH(launch_t, a, grid, stream)
 }
 
-int walk_occupancy(int app, int sampler, bool exact) { FW_DISPATCH(occupancy_t) }
+int walk_occupancy(int app, int sampler, int mode) { FW_DISPATCH(occupancy_t) }
 
 }  // namespace fw

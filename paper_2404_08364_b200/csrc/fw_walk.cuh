@@ -73,14 +73,20 @@ struct WalkArgs {
     // its paths back while the walk continues.
     unsigned *done;
     uint64_t piece_q;
+    // mode 2: certified accept tests; slack = 2^-50 (FW_CERT_SLACK scales it
+    // up in tests to force the ordered re-run)
+    double cert_slack;
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };
 
 constexpr uint32_t kSchemaInline = 16;  // metapath schemas up to this length ride in the args
 
-cudaError_t launch_walk(const WalkArgs &a, int app, int sampler, bool exact, int grid,
+// mode: 0 ordered (the reference's summation order), 1 exact (tree scans,
+// every partial sum exact), 2 certified (DPRS: tree scans + certified accept
+// tests, ambiguous steps re-run in order)
+cudaError_t launch_walk(const WalkArgs &a, int app, int sampler, int mode, int grid,
                         cudaStream_t stream);
-int walk_occupancy(int app, int sampler, bool exact);
+int walk_occupancy(int app, int sampler, int mode);
 
 }  // namespace fw

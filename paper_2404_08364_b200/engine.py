@@ -169,7 +169,11 @@ class RunStats:
     sampled_steps: int = 0
     alg_bytes: int = 0
     kernel_ms: float = 0.0
-    exact_order: bool = False
+    exact_order: bool = False  # tree-order scans ran (modes "exact" and "certified")
+    # "sequential": the reference's summation order replayed; "exact": every
+    # partial sum exact, tree scans; "certified": tree scans with certified
+    # accept tests, ambiguous steps re-run in order
+    summation: str = "sequential"
 
 
 # ---------------------------------------------------------------------------
@@ -431,14 +435,19 @@ def _walk_batch(sess, starts, base_qid, app, eng, seed, seq, lens, totals):
         totals["aux_allocations"] = max(totals["aux_allocations"], st.aux_allocations)
         totals["per_device"][i] += cnt
         totals["exact_order"] = bool(st.exact_order)
+        totals["summation"] = _SUMMATION.get(int(st.exact_order), "sequential")
     totals["kernel_ms"] += batch_ms  # batches run one after another
     totals["aux_bytes"] = max(totals["aux_bytes"], aux)
+
+
+_SUMMATION = {0: "sequential", 1: "exact", 2: "certified"}
 
 
 def _new_totals(parts=1):
     t = {f: 0 for f in _lib.ST_FIELDS}
     t["kernel_ms"] = 0.0
     t["exact_order"] = False
+    t["summation"] = "sequential"
     t["aux_bytes"] = 0
     t["aux_allocations"] = 0
     t["per_device"] = [0] * parts
@@ -533,7 +542,8 @@ def run(g, starts, app_cfg, eng_cfg, seed=0, sink=None, keep_query_ids=False, on
         aux_bytes=int(totals["aux_bytes"]), aux_allocations=int(totals["aux_allocations"]),
         completed=n, per_worker_completed=_per_worker(totals["per_device"], eng_cfg.workers),
         sampled_steps=int(totals["sampled_steps"]), alg_bytes=int(totals["alg_bytes"]),
-        kernel_ms=float(totals["kernel_ms"]), exact_order=bool(totals["exact_order"]))
+        kernel_ms=float(totals["kernel_ms"]), exact_order=bool(totals["exact_order"]),
+        summation=totals["summation"])
     if keep_query_ids:
         stats.completed_query_ids = np.arange(base_qid, base_qid + n, dtype=np.int64)
     return stats

@@ -8,4 +8,4 @@ cp "$1" $D/p/csrc/fw_walk.cu
   -Xcompiler -fPIC -shared $XFLAGS -o paper_2404_08364_b200/libflowwalk_$2.so \
   $D/p/csrc/fw_api.cu $D/p/csrc/fw_walk.cu $D/p/csrc/fw_trials.cu
 rm -rf $D
-/usr/local/cuda/bin/cuobjdump -res-usage paper_2404_08364_b200/libflowwalk_$2.so 2>/dev/null | grep -A1 "walk_kernelILi2ELi1ELb1" | tail -1
+/usr/local/cuda/bin/cuobjdump -res-usage paper_2404_08364_b200/libflowwalk_$2.so 2>/dev/null | grep -A1 "walk_kernelILi2ELi1ELi1" | tail -1

@@ -56,6 +56,8 @@ def parse_args():
                    choices=["node2vec", "deepwalk", "ppr", "metapath"])
     p.add_argument("--length", type=int, default=None)
     p.add_argument("--queries", default="all", help="all | hub (PPR config)")
+    p.add_argument("--a", type=float, default=2.0, help="node2vec return parameter (p)")
+    p.add_argument("--b", type=float, default=0.5, help="node2vec in-out parameter (q)")
     p.add_argument("--weights", choices=["uniform", "lognormal"], default="uniform",
                    help="edge weights: U[1,5) (BASELINE) or log-normal(0, 1) as "
                         "graph.py:183-188 draws them (seed 2): sums that round, the "
@@ -81,7 +83,7 @@ def parse_args():
 def app_config(args):
     import paper_2404_08364_b200 as fw
     if args.app == "node2vec":
-        return fw.AppConfig(app="node2vec", length=args.length or 80, a=2.0, b=0.5)
+        return fw.AppConfig(app="node2vec", length=args.length or 80, a=args.a, b=args.b)
     if args.app == "deepwalk":
         return fw.AppConfig(app="deepwalk", length=args.length or 80)
     if args.app == "ppr":
@@ -95,7 +97,7 @@ def metric_name(args):
 
 
 def workload_name(args, app):
-    extra = {"node2vec": " p=2 q=0.5", "ppr": " stop 0.2", "metapath": " schema 0..4",
+    extra = {"node2vec": f" p={args.a:g} q={args.b:g}", "ppr": " stop 0.2", "metapath": " schema 0..4",
              "deepwalk": " weighted"}[args.app]
     q = "all queries at the max-degree vertex" if args.queries == "hub" else "one query per vertex"
     wt = ", log-normal weights" if args.weights == "lognormal" else ""
@@ -176,6 +178,23 @@ def profiled_traffic(workload, alg_bytes):
             f"ncu --set full of a {d['queries']}-query launch ({d['report']}): "
             f"{d['dram_bytes'] / d['alg_bytes']:.3f} DRAM bytes per algorithmic byte, "
             f"scaled to this launch")
+
+
+def profiled_counters(workload):
+    """What bounds the kernel, from the same committed capture: issue-slot
+    use, L2 sector throughput and global-load sector efficiency."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as fh:
+            d = json.load(fh).get(workload) or {}
+    except (OSError, ValueError):
+        return None
+    if "issue_pct" not in d:
+        return None
+    return {"issue_slots_busy_pct": d["issue_pct"],
+            "l2_sector_throughput_pct_of_peak": d.get("l2_sector_pct_of_peak"),
+            "global_load_bytes_used_per_32B_sector": d.get("sector_bytes_used"),
+            "dram_bytes_per_algorithmic_byte": d["dram_bytes"] / d["alg_bytes"],
+            "report": d["report"]}
 
 
 # ---------------------------------------------------------------------------
@@ -486,6 +505,20 @@ def bench_ours(args):
                 "traffic": traffic, "traffic_basis": traffic_basis,
                 "alg_bytes_per_launch": alg_bytes // args.steps,
                 "kernel": "fw::walk_kernel (persistent, 1 launch per step)"}
+    if traffic:
+        # the measured DRAM rate next to the algorithmic one: frac counts the
+        # bytes SURVEY 8(d) defines, much of which the walks re-read from L2
+        roofline["dram_achieved"] = traffic / mean_launch_s / 1e9
+        roofline["dram_frac"] = roofline["dram_achieved"] / peak
+    counters = profiled_counters(workload)
+    if counters:
+        roofline["binding"] = ("issue: instruction issue, not HBM, limits this kernel "
+                               "(DESIGN.md 3.3); DRAM and L2 run well below their peaks")
+        roofline["counters"] = counters
+    if roofline["frac"] > 1.0:
+        roofline["note"] = ("algorithmic bytes exceed the HBM peak: the walks' adjacency is "
+                            "L2-resident (re-read from the 126 MB L2), so frac is not an "
+                            "HBM fraction here; see dram_frac and counters")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

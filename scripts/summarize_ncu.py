@@ -63,6 +63,14 @@ METRICS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
     ("smsp__average_warp_latency_issue_stalled_long_scoreboard", None),
+    ("smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio",
+     "global-load sector efficiency: bytes used per 32-B sector"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global-load L1 sectors"),
+    ("memory_l2_theoretical_sectors_global", "L2 sectors requested by global accesses"),
+    ("memory_l2_theoretical_sectors_global_ideal", "  ... ideal (fully coalesced)"),
+    ("lts__t_sectors.sum", "L2 sectors (all)"),
+    ("lts__t_sectors.sum.pct_of_peak_sustained_elapsed", "L2 sector throughput % of peak"),
+    ("smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio", None),
 ]
 
 
@@ -99,8 +107,22 @@ def full(rep, out, traffic_key=None, alg_bytes=None, queries=None):
             if traffic_key:
                 p = os.path.join(ROOT, "profiles", "walk_traffic.json")
                 cur = json.load(open(p)) if os.path.exists(p) else {}
+                def num(key):
+                    try:
+                        return float(d.get(key, "").replace(",", ""))
+                    except ValueError:
+                        return None
                 cur[traffic_key] = {"dram_bytes": tb, "alg_bytes": alg_bytes, "queries": queries,
-                                    "report": os.path.basename(rep)}
+                                    "report": os.path.basename(rep),
+                                    "kernel_ms": num("gpu__time_duration.sum"),
+                                    "l2_sectors": num("lts__t_sectors.sum"),
+                                    "l2_sector_pct_of_peak": num(
+                                        "lts__t_sectors.sum.pct_of_peak_sustained_elapsed"),
+                                    "sector_bytes_used": num(
+                                        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio"),
+                                    "issue_pct": num(
+                                        "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                    "warp_inst": num("smsp__inst_executed.sum")}
                 json.dump(cur, open(p, "w"), indent=1)
     print(open(out).read())
 

@@ -534,12 +534,11 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     const bool fc = force_cert && force_cert[0] == '1';
     const bool exact = eng->order_mode == FW_ORDER_AUTO && !fc &&
                        exact_order_ok(g->info, *app, &G, &xmax);
-    // certified mode (DPRS over weights whose sums round, e.g. log-normal):
+    // certified mode (weights whose sums round, e.g. log-normal):
     // tree-order scans with certified accept tests; needs nonnegative finite
     // weights and sums far from overflow (cert_accept's bound)
     int mode = exact ? 1 : 0;
-    if (!exact && eng->order_mode == FW_ORDER_AUTO && eng->sampler_id == FW_SAMPLER_DPRS &&
-        app->weighted && !g->info.bad_weights) {
+    if (!exact && eng->order_mode == FW_ORDER_AUTO && app->weighted && !g->info.bad_weights) {
         double fmax = 1.0;
         if (app->app_id == FW_APP_NODE2VEC) fmax = std::max({1.0, app->inv_a, app->inv_b});
         const double tot = (double)g->info.max_degree * fmax * (double)g->info.max_weight;

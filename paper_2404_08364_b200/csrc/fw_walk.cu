@@ -118,6 +118,35 @@ __device__ __forceinline__ int cert_accept(double r, double P, double w, double 
 }
 constexpr uint32_t kCertFallback = 0xFFFFFFFFu;  // "re-run this step in order"
 
+// The accept test of element idx1 - 1: exact (fl(r * P) < w, _kernels.py:421,
+// 457) or, CERT, certified against the bound tot with ti terms in the sums
+// (ambiguous -> amb).
+template <bool CERT>
+__device__ __forceinline__ void accept_test(double r, double P, double w, uint32_t idx1,
+                                            double tot, uint32_t ti, double slack,
+                                            uint32_t &cand, uint32_t &amb) {
+    if constexpr (CERT) {
+        if (w > 0.0) {
+            const int c = cert_accept(r, P, w, tot, ti, slack);
+            if (c == 1) cand = idx1;
+            else if (c == 2) amb = idx1;
+        }
+    } else if (w > 0.0 && __dmul_rn(r, P) < w) {
+        cand = idx1;
+    }
+}
+
+// Prefilter threshold for a batch of elements starting at prefix `base`.
+// CERT kernels bound w by the batch's own largest weight (any upper bound on
+// the tested w keeps the prefilter exact) instead of the graph-wide maximum:
+// log-normal weights span ~2^10, so the global bound lets far more elements
+// through to the full draw.
+template <bool CERT>
+__device__ __forceinline__ uint32_t batch_thr(const WalkArgs &a, double base, double wmax_b) {
+    if constexpr (CERT) return accept_thr_f(__double2float_ru(wmax_b), (float)base);
+    else return accept_thr(a.accept_wmax, base);
+}
+
 template <int APP>
 __device__ __forceinline__ double elem_weight(const WalkArgs &a, const StepCtx &s, uint32_t i) {
     const int64_t e = s.elo + i;
@@ -200,13 +229,18 @@ __device__ __forceinline__ double lane_excl_scan(double lsum, double &ecarry, in
     return excl;
 }
 
-template <int APP, uint32_t KC = 0>
+// CERT: certified accept tests against the step total tot (the lane's
+// exclusive prefix comes from a tree scan); amb = last ambiguous element + 1.
+template <int APP, uint32_t KC = 0, bool CERT = false>
 __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const StepCtx &s,
                                                     uint32_t j, uint32_t k, double run,
-                                                    bool staged, uint32_t woff) {
+                                                    bool staged, uint32_t woff,
+                                                    [[maybe_unused]] double tot = 0.0,
+                                                    [[maybe_unused]] uint32_t *amb_out = nullptr) {
     if (KC) k = KC;
     const float *stage = reinterpret_cast<const float *>(fw_smem) + woff;
     uint32_t cand = 0;
+    [[maybe_unused]] uint32_t amb = 0;
     uint64_t word = lane_base(a, s, j);
     const uint32_t deg = s.deg;
     // Accept prefilter (as in dprs_n2v_pow2): element accepted => r <
@@ -216,14 +250,16 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
     uint32_t i = j;
     if (staged) {
         for (; i + 3 * k < deg; i += 4 * k) {
-            const uint32_t thr = accept_thr(a.accept_wmax, run);
+            const uint32_t thr = batch_thr<CERT>(
+                a, run, CERT ? fmaxf(fmaxf(stage[i], stage[i + k]),
+                                     fmaxf(stage[i + 2 * k], stage[i + 3 * k])) : 0.0);
 #pragma unroll
             for (int r = 0; r < 4; r++, word += GOLDEN) {
                 const double wv = (double)stage[i + r * k];
                 run = __dadd_rn(run, wv);
                 if (mix64_yhi(word) <= thr) {
                     const double u = u01_word(word);
-                    if (wv > 0.0 && __dmul_rn(u, run) < wv) cand = i + r * k + 1;
+                    accept_test<CERT>(u, run, wv, i + r * k + 1, tot, i + r * k + k, a.cert_slack, cand, amb);
                 }
             }
         }
@@ -231,7 +267,7 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
             const double wv = (double)stage[i];
             run = __dadd_rn(run, wv);
             const double r = u01_word(word);
-            if (wv > 0.0 && __dmul_rn(r, run) < wv) cand = i + 1;
+            accept_test<CERT>(r, run, wv, i + 1, tot, i + k, a.cert_slack, cand, amb);
         }
     } else {
         if constexpr (APP != APP_NODE2VEC) {
@@ -243,14 +279,19 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
 #pragma unroll
                     for (int r = 0; r < 8; r++)
                         w[r] = a.weighted ? ldg(a.w + s.elo + i + (uint32_t)r * k) : 1.0f;
-                    const uint32_t thr = accept_thr(a.accept_wmax, run);
+                    float wm8 = 0.0f;
+                    if constexpr (CERT) {
+#pragma unroll
+                        for (int r = 0; r < 8; r++) wm8 = fmaxf(wm8, w[r]);
+                    }
+                    const uint32_t thr = batch_thr<CERT>(a, run, wm8);
 #pragma unroll
                     for (int r = 0; r < 8; r++, word += GOLDEN) {
                         const double wv = (double)w[r];
                         run = __dadd_rn(run, wv);
                         if (mix64_yhi(word) <= thr) {
                             const double u = u01_word(word);
-                            if (wv > 0.0 && __dmul_rn(u, run) < wv) cand = i + r * k + 1;
+                            accept_test<CERT>(u, run, wv, i + r * k + 1, tot, i + r * k + k, a.cert_slack, cand, amb);
                         }
                     }
                 }
@@ -258,13 +299,14 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
             for (; i + 3 * k < deg; i += 4 * k) {
                 double x[4];
                 weights4<APP, KC>(a, s, i, k, x);
-                const uint32_t thr = accept_thr(a.accept_wmax, run);
+                const uint32_t thr =
+                    batch_thr<CERT>(a, run, CERT ? fmax(fmax(x[0], x[1]), fmax(x[2], x[3])) : 0.0);
 #pragma unroll
                 for (int r = 0; r < 4; r++, word += GOLDEN) {
                     run = __dadd_rn(run, x[r]);
                     if (mix64_yhi(word) <= thr) {
                         const double u = u01_word(word);
-                        if (x[r] > 0.0 && __dmul_rn(u, run) < x[r]) cand = i + r * k + 1;
+                        accept_test<CERT>(u, run, x[r], i + r * k + 1, tot, i + r * k + k, a.cert_slack, cand, amb);
                     }
                 }
             }
@@ -273,9 +315,10 @@ __device__ __forceinline__ uint32_t zprs_lane_pass2(const WalkArgs &a, const Ste
             const double wv = elem_weight<APP>(a, s, i);
             run = __dadd_rn(run, wv);
             const double r = u01_word(word);
-            if (wv > 0.0 && __dmul_rn(r, run) < wv) cand = i + 1;
+            accept_test<CERT>(r, run, wv, i + 1, tot, i + k, a.cert_slack, cand, amb);
         }
     }
+    if constexpr (CERT) *amb_out = amb;
     return cand;
 }
 
@@ -323,9 +366,14 @@ __device__ __forceinline__ double zprs_lane_pass1(const WalkArgs &a, const StepC
 }
 
 // KC: compile-time lane width (32 / 256, the reference's defaults) or 0.
-template <int APP, bool EXACT, uint32_t KC = 0>
+// CERT (with EXACT): tree lane scan and certified accept tests; the winner
+// (highest lane with a candidate, its last accepted element) is certain
+// unless a lane above it, or the winner after its candidate, holds an
+// ambiguous test -- then kCertFallback (the caller re-runs the step in order).
+template <int APP, bool EXACT, uint32_t KC = 0, bool CERT = false>
 __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, int lane,
                               uint32_t woff) {
+    static_assert(!CERT || EXACT, "certified ZPRS uses the tree lane scan");
     if (KC) k = KC;
     const uint32_t deg = s.deg;
     const uint32_t nl = k < deg ? k : deg;
@@ -336,6 +384,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
         const uint32_t j = lane;
         double lsum = 0.0;
         uint32_t cand = 0;
+        [[maybe_unused]] uint32_t amb = 0;
         double ecarry = 0.0;
         if (APP == APP_METAPATH && staged) {
             // Most MetaPath weights are 0 (label filter).  A zero weight adds
@@ -378,17 +427,24 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
                     const uint32_t c = cst[j + k * x];
                     run = __dadd_rn(run, wv);
                     const double r = u01_word(base + (uint64_t)c * GOLDEN);
-                    if (__dmul_rn(r, run) < wv) cand = c * k + j + 1;
+                    accept_test<CERT>(r, run, wv, c * k + j + 1, ecarry, c * k + j + k,
+                                      a.cert_slack, cand, amb);
                 }
             }
         } else {
             if (j < nl) lsum = zprs_lane_pass1<APP, KC>(a, s, j, k, staged, stage);
             const double excl = lane_excl_scan<APP, EXACT>(lsum, ecarry, lane);
-            cand = j < nl ? zprs_lane_pass2<APP, KC>(a, s, j, k, excl, staged, woff) : 0;
+            cand = j < nl ? zprs_lane_pass2<APP, KC, CERT>(a, s, j, k, excl, staged, woff,
+                                                            ecarry, &amb)
+                          : 0;
         }
         const unsigned m = __ballot_sync(FULL, cand > 0);
         const uint32_t c = __shfl_sync(FULL, cand, m ? 31 - __clz(m) : 0);
         __syncwarp();
+        if constexpr (CERT) {  // ambiguity at or above the winner
+            const unsigned bad = __ballot_sync(FULL, amb > cand);
+            if (bad >> (m ? 31 - __clz(m) : 0)) return kCertFallback;
+        }
         return m ? c : 0;
     }
     if (nl <= 256) {  // up to 8 groups: lane sums -> exclusive prefixes in smem
@@ -404,8 +460,18 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
         uint32_t best = 0;
         for (int g = (int)ng - 1; g >= 0; g--) {
             const uint32_t j = g * 32 + lane;
-            const uint32_t cand = j < nl ? zprs_lane_pass2<APP, KC>(a, s, j, k, E[j], staged, woff) : 0;
+            [[maybe_unused]] uint32_t amb = 0;
+            const uint32_t cand = j < nl ? zprs_lane_pass2<APP, KC, CERT>(a, s, j, k, E[j], staged,
+                                                                          woff, ecarry, &amb)
+                                         : 0;
             const unsigned m = __ballot_sync(FULL, cand > 0);
+            if constexpr (CERT) {
+                const unsigned bad = __ballot_sync(FULL, amb > cand);
+                if (bad >> (m ? 31 - __clz(m) : 0)) {
+                    best = kCertFallback;
+                    break;
+                }
+            }
             if (m) {
                 best = __shfl_sync(FULL, cand, 31 - __clz(m));
                 break;
@@ -414,6 +480,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
         __syncwarp();
         return best;
     }
+    if constexpr (CERT) return kCertFallback;  // k > 256: the step total comes too late
     // k > 256: group by group, upward (generic k, correctness path)
     double ecarry = 0.0;
     uint32_t best = 0;
@@ -462,7 +529,7 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
         for (uint32_t t0 = 0; t0 < deg; t0 += 32, word += GOLDEN) {
             const uint32_t i = t0 + lane;
             const double wv = i < deg ? elem_weight<APP>(a, s, i) : 0.0;
-            const uint32_t thr = accept_thr(a.accept_wmax, carry);  // prefilter
+            const uint32_t thr = batch_thr<CERT>(a, carry, wv);  // prefilter
             const double incl = warp_incl_scan(wv, lane);
             const double P = __dadd_rn(carry, incl);
             const double nc = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
@@ -484,7 +551,7 @@ __device__ uint32_t dprs_warp_exact(const WalkArgs &a, const StepCtx &s, uint32_
                 if (t0 < deg) {  // warp-uniform
                     const uint32_t i = t0 + lane;
                     const double wv = i < deg ? elem_weight<APP>(a, s, i) : 0.0;
-                    const uint32_t thr = accept_thr(a.accept_wmax, carry);  // prefilter
+                    const uint32_t thr = batch_thr<CERT>(a, carry, wv);  // prefilter
                     const double incl = warp_incl_scan(wv, lane);
                     const double P = __dadd_rn(carry, incl);
                     const double nc = __dadd_rn(carry, __shfl_sync(FULL, incl, 31));
@@ -1082,7 +1149,8 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             // prefilter threshold from the tile's starting carry (<= every
             // lane's base, so the bound below stays valid); it does not wait
             // for the scan
-            const uint32_t thr = accept_thr(a.accept_wmax, carry);
+            const uint32_t thr =
+                batch_thr<CERT>(a, carry, CERT ? fmax(fmax(wv[0], wv[1]), fmax(wv[2], wv[3])) : 0.0);
             const double incl = warp_incl_scan_p(p3);
             const double base = __dadd_rn(carry, __dadd_rn(incl, -p3));  // exact
             carry = __dadd_rn(carry, shfl_d(incl, 31));
@@ -1292,8 +1360,8 @@ __device__ __forceinline__ void stat_add(unsigned long long *st, int idx, long l
 // The persistent walker.
 // ---------------------------------------------------------------------------
 // MODE: 0 = the reference's summation order replayed (ordered kernels),
-// 1 = exact (every partial sum exact: tree scans), 2 = certified (DPRS only:
-// tree scans with certified accept tests, ambiguous steps re-run in order).
+// 1 = exact (every partial sum exact: tree scans), 2 = certified (tree scans
+// with certified accept tests, ambiguous steps re-run in order).
 template <int APP, int SAMPLER, int MODE>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks(APP))
 walk_kernel(const __grid_constant__ WalkArgs a) {
@@ -1403,7 +1471,19 @@ walk_kernel(const __grid_constant__ WalkArgs a) {
             } else {
                 // compile-time lane widths (immediate load offsets): +11-13%
                 // for DeepWalk / PPR; MetaPath measured 14% slower with them
-                if constexpr (APP == APP_METAPATH)
+                if constexpr (CERT) {
+                    // certified: tree lane scan; an ambiguous step re-runs
+                    // with the reference's sequential lane scan
+                    if constexpr (APP == APP_METAPATH) {
+                        sel = zprs_warp<APP, true, 0, true>(a, s, k, lane, woff);
+                        if (sel == kCertFallback) sel = zprs_warp<APP, false>(a, s, k, lane, woff);
+                    } else {
+                        sel = k == 32    ? zprs_warp<APP, true, 32, true>(a, s, k, lane, woff)
+                              : k == 256 ? zprs_warp<APP, true, 256, true>(a, s, k, lane, woff)
+                                         : zprs_warp<APP, true, 0, true>(a, s, k, lane, woff);
+                        if (sel == kCertFallback) sel = zprs_warp<APP, false>(a, s, k, lane, woff);
+                    }
+                } else if constexpr (APP == APP_METAPATH)
                     sel = zprs_warp<APP, EXACT>(a, s, k, lane, woff);
                 else
                     sel = k == 32    ? zprs_warp<APP, EXACT, 32>(a, s, k, lane, woff)
@@ -1478,11 +1558,11 @@ static int occupancy_t() {
     return nb;
 }
 
-// mode 2 exists for DPRS only (the host never asks for certified ZPRS)
 #define FW_DISPATCH_APP(FN, APP, ...)                                                \
     if (sampler == SAMPLER_ZPRS) {                                                   \
         if (mode == 0) return FN<APP, 0, 0>(__VA_ARGS__);                            \
-        return FN<APP, 0, 1>(__VA_ARGS__);                                           \
+        if (mode == 1) return FN<APP, 0, 1>(__VA_ARGS__);                            \
+        return FN<APP, 0, 2>(__VA_ARGS__);                                           \
     }                                                                                \
     if (mode == 0) return FN<APP, 1, 0>(__VA_ARGS__);                                \
     if (mode == 1) return FN<APP, 1, 1>(__VA_ARGS__);                                \

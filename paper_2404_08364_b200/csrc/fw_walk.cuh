@@ -83,7 +83,7 @@ struct WalkArgs {
 constexpr uint32_t kSchemaInline = 16;  // metapath schemas up to this length ride in the args
 
 // mode: 0 ordered (the reference's summation order), 1 exact (tree scans,
-// every partial sum exact), 2 certified (DPRS: tree scans + certified accept
+// every partial sum exact), 2 certified (tree scans + certified accept
 // tests, ambiguous steps re-run in order)
 cudaError_t launch_walk(const WalkArgs &a, int app, int sampler, int mode, int grid,
                         cudaStream_t stream);

@@ -1,7 +1,7 @@
-"""Certified summation (walk mode 2): DPRS over weights whose fp64 partial
-sums round (log-normal, non-dyadic), with tree-order scans and certified
-accept tests instead of the reference's sequential sums
-(_kernels.py:404-424).  Paths must equal the reference's bit for bit, both on
+"""Certified summation (walk mode 2): DPRS and ZPRS over weights whose fp64
+partial sums round (log-normal, non-dyadic), with tree-order scans and
+certified accept tests instead of the reference's sequential sums
+(_kernels.py:404-424, 436-457).  Paths must equal the reference's bit for bit, both on
 the fast path and when an ambiguous accept test re-runs the step in order
 (forced here by widening the ambiguity band with FW_CERT_SLACK)."""
 
@@ -77,6 +77,10 @@ def s16_lognormal():
     (dict(app="node2vec", length=40, a=3.0, b=0.7), "auto"),  # fp64 factors
     (dict(app="deepwalk", length=80), "dprs"),
     (dict(app="ppr", length=80, stop_prob=0.2), "dprs"),
+    (dict(app="deepwalk", length=80), "auto"),  # ZPRS
+    (dict(app="ppr", length=80, stop_prob=0.2), "auto"),
+    (dict(app="metapath", length=5, schema=(0, 1, 2, 3, 4)), "auto"),
+    (dict(app="node2vec", length=40, a=2.0, b=0.5), "zprs"),
 ])
 def test_rmat_s16_lognormal_matches_oracle(s16_lognormal, app, sampler, slack):
     g = s16_lognormal
@@ -111,17 +115,21 @@ def test_certified_equals_ordered_kernels(s16_lognormal):
     np.testing.assert_array_equal(seq_c, seq_o)
 
 
-def test_zprs_lognormal_stays_sequential(s16_lognormal):
-    """Certification covers DPRS; ZPRS over rounding sums keeps the ordered
-    lane scan (and is still bit-exact)."""
+def test_zprs_hub_groups_certified(s16_lognormal):
+    """k = 256 hub steps (8 lane groups, pass 2 from the top group down) and
+    PPR's 8-element batches under certification, with forced re-runs."""
     g = s16_lognormal
-    starts = np.arange(0, g.vertex_count, 16, dtype=np.int64)
-    app = dict(app="deepwalk", length=40)
-    with _env(FW_FORCE_CERT="1"):
-        seq, ln, st = _run(g, starts, fw.AppConfig(**app), fw.EngineConfig(replay=True))
-    assert st.summation == "sequential"
-    oseq, oln, _ = oracle.walk(g.offsets, g.targets, g.weights, g.labels, starts, **app)
-    np.testing.assert_array_equal(seq, oseq)
+    hub = g.max_degree_vertex()
+    starts = np.full(4096, hub, np.int64)
+    for slack in (None, "40"):
+        for app in (dict(app="deepwalk", length=20), dict(app="ppr", length=80, stop_prob=0.2)):
+            with _env(FW_FORCE_CERT="1", **({"FW_CERT_SLACK": slack} if slack else {})):
+                seq, ln, st = _run(g, starts, fw.AppConfig(**app), fw.EngineConfig(replay=True))
+            assert st.summation == "certified"
+            oseq, oln, ost = oracle.walk(g.offsets, g.targets, g.weights, g.labels, starts, **app)
+            np.testing.assert_array_equal(ln, oln)
+            np.testing.assert_array_equal(seq, oseq)
+            assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()
 
 
 def test_wide_lognormal_selects_certified_on_its_own():

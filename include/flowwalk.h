@@ -57,7 +57,11 @@ enum { FW_APP_DEEPWALK = 0, FW_APP_PPR = 1, FW_APP_NODE2VEC = 2, FW_APP_METAPATH
 enum { FW_SAMPLER_ZPRS = 0, FW_SAMPLER_DPRS = 1 };
 /* fp64 summation order: auto picks tree-order scans when every partial sum
  * is provably exact (so any order is bit-identical to the reference's
- * sequential order), else the reference's sequential order. */
+ * sequential order); otherwise, for nonnegative finite weights, tree-order
+ * scans with certified accept tests (a step whose test cannot be decided from
+ * the error bound is re-run in the reference's order), else the
+ * reference's sequential order.  SEQUENTIAL always replays the reference's
+ * order.  fw_stats.exact_order reports 1 (exact), 2 (certified) or 0. */
 enum { FW_ORDER_AUTO = 0, FW_ORDER_SEQUENTIAL = 1 };
 
 typedef struct fw_graph fw_graph;

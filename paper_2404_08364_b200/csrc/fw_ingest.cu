@@ -14,10 +14,13 @@
 // The sort is reduce-then-scan per 8-bit digit over a persistent grid: each
 // CTA owns one contiguous segment of the keys, (1) histograms it, (2) one
 // scan turns the [digit][CTA] table into global output offsets, (3) the CTA
-// re-reads its segment tile by tile, in order, and ranks each key within its
-// digit by warp match + per-warp counters (row order, then warp order), so
-// equal digits keep their input order: every pass is stable, hence the
-// whole sort is (the lexsort tie rule).  Passes whose digit is constant over
+// re-reads its segment tile by tile, in order, ranks each key within its
+// digit by warp match + per-warp counters (row order, then warp order), and
+// stages the tile in shared memory in digit order so each digit's run is
+// stored with coalesced writes.  Equal digits keep their input order: every
+// pass is stable, hence the whole sort is (the lexsort tie rule).  Only keys
+// move unless weights or labels come along (then a 32-bit value: the weight
+// itself when there are no labels, else the input index for a gather).  Passes whose digit is constant over
 // all keys are skipped.  HBM-bound integer work: no tensor cores.
 #include <cuda_runtime.h>
 #include <fcntl.h>
@@ -53,6 +56,7 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int kThreads = 256, kWarps = kThreads / 32, kRows = 8;
 constexpr int kTile = kWarps * kRows * 32;  // keys per scatter tile
 constexpr int kRadix = 256;
+static_assert(kThreads == kRadix, "k_scatter: one thread per digit");
 
 __global__ void k_max_id(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
                          uint64_t m, unsigned *out) {
@@ -64,13 +68,15 @@ __global__ void k_max_id(const uint32_t *__restrict__ a, const uint32_t *__restr
     if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
+// vals: the input index (labels to gather), or -- weights without labels --
+// the weight's bits themselves, so the sorted weights need no random gather
 __global__ void k_make_keys(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
-                            uint64_t m, int bv, uint64_t *__restrict__ keys,
-                            uint32_t *__restrict__ vals) {
+                            uint64_t m, int bv, const float *__restrict__ w_carry,
+                            uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x) {
         keys[i] = ((uint64_t)src[i] << bv) | dst[i];
-        vals[i] = (uint32_t)i;
+        if (vals) vals[i] = w_carry ? __float_as_uint(w_carry[i]) : (uint32_t)i;
     }
 }
 
@@ -124,21 +130,33 @@ __global__ void __launch_bounds__(1024) k_scan(uint32_t *t, uint32_t n, uint32_t
     }
 }
 
-// (3) stable scatter of the CTA's segment
+// (3) stable scatter of the CTA's segment, staged through shared memory.
+// Per tile: keys are ranked within their digit (warp match, then warp order),
+// written to shared memory in digit-sorted order, and only then stored to
+// global memory by consecutive threads -- each digit's run of the tile goes
+// out as contiguous, coalesced stores instead of 32 scattered sectors per warp
+// store.  Order within a digit is row-major input order, so the pass is
+// stable.  VALS: carry the 32-bit input index (weights/labels to gather).
+template <bool VALS>
 __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t *__restrict__ kin,
                                                       const uint32_t *__restrict__ vin, uint64_t m,
                                                       uint64_t seg, int shift,
                                                       const uint32_t *__restrict__ offs,
                                                       uint64_t *__restrict__ kout,
                                                       uint32_t *__restrict__ vout) {
-    __shared__ uint32_t run[kRadix];
+    __shared__ uint32_t run[kRadix];     // this CTA's global cursor per digit
+    __shared__ uint32_t tstart[kRadix];  // tile-local start of each digit
+    __shared__ uint32_t wsum[kWarps];
     __shared__ uint32_t wc[kWarps][kRadix];
+    __shared__ uint64_t sk[kTile];
+    __shared__ uint32_t sv[VALS ? kTile : 1];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1;
     for (int d = threadIdx.x; d < kRadix; d += kThreads)
         run[d] = offs[(uint64_t)d * gridDim.x + blockIdx.x];
     const uint64_t lo = blockIdx.x * seg, hi = min(m, lo + seg);
     for (uint64_t t0 = lo; t0 < hi; t0 += kTile) {
+        const uint32_t tn = (uint32_t)(hi - t0 < (uint64_t)kTile ? hi - t0 : (uint64_t)kTile);
         for (int d = lane; d < kRadix; d += 32) wc[w][d] = 0;
         __syncwarp();
         uint64_t key[kRows];
@@ -148,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t *__restrict
             const uint64_t i = t0 + (uint64_t)(w * kRows + r) * 32 + lane;
             const bool ok = i < hi;
             key[r] = ok ? kin[i] : 0;
-            val[r] = ok ? vin[i] : 0;
+            val[r] = (VALS && ok) ? vin[i] : 0;
             dig[r] = ok ? (uint32_t)((key[r] >> shift) & 0xFF) : kRadix;  // 256: past the end
         }
 #pragma unroll
@@ -161,42 +179,66 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t *__restrict
             rank[r] = base + __popc(peers & lt);
         }
         __syncthreads();
-        for (int d = threadIdx.x; d < kRadix; d += kThreads) {  // warps in order
-            uint32_t acc = run[d];
+        // per digit (thread d): warp-order prefixes within the digit and the
+        // tile total; then an exclusive scan of the totals over the digits
+        uint32_t tot = 0;
+        {
+            const int d = threadIdx.x;  // kThreads == kRadix
 #pragma unroll
             for (int x = 0; x < kWarps; x++) {
                 const uint32_t c = wc[x][d];
-                wc[x][d] = acc;
-                acc += c;
+                wc[x][d] = tot;
+                tot += c;
             }
-            run[d] = acc;
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) wsum[w] = incl;
+            __syncthreads();
+            uint32_t wofs = 0;
+            for (int x = 0; x < w; x++) wofs += wsum[x];
+            tstart[d] = wofs + incl - tot;
         }
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < kRows; r++) {
             if (dig[r] < kRadix) {
-                const uint32_t pos = wc[w][dig[r]] + rank[r];
-                kout[pos] = key[r];
-                vout[pos] = val[r];
+                const uint32_t lp = tstart[dig[r]] + wc[w][dig[r]] + rank[r];
+                sk[lp] = key[r];
+                if (VALS) sv[lp] = val[r];
             }
         }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < tn; i += kThreads) {
+            const uint64_t k = sk[i];
+            const uint32_t d = (uint32_t)((k >> shift) & 0xFF);
+            const uint32_t pos = run[d] + (i - tstart[d]);
+            kout[pos] = k;
+            if (VALS) vout[pos] = sv[i];
+        }
+        __syncthreads();
+        run[threadIdx.x] += tot;  // kThreads == kRadix: thread d owns digit d
         __syncthreads();
     }
 }
 
 // CSR arrays from the sorted keys: targets, and weights/labels gathered by
 // the carried input index (a thread per key) ...
+// (carried: idx holds the sorted weights' bits, see k_make_keys)
 __global__ void k_csr_edges(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ idx,
-                            uint64_t m, int bv, const float *__restrict__ w_in,
+                            bool carried, uint64_t m, int bv, const float *__restrict__ w_in,
                             const uint8_t *__restrict__ l_in, uint32_t *__restrict__ tgt,
                             float *__restrict__ w_out, uint8_t *__restrict__ l_out) {
     const uint64_t mask = (1ull << bv) - 1;
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
          e += (uint64_t)gridDim.x * blockDim.x) {
         tgt[e] = (uint32_t)(keys[e] & mask);
-        const uint32_t j = idx[e];
-        if (w_out) w_out[e] = w_in ? w_in[j] : 1.0f;
-        if (l_out) l_out[e] = l_in ? l_in[j] : 0;
+        const uint32_t j = idx ? idx[e] : 0;
+        if (w_out) w_out[e] = carried ? __uint_as_float(j) : (w_in ? w_in[j] : 1.0f);
+        if (l_out) l_out[e] = (l_in && !carried) ? l_in[j] : 0;
     }
 }
 
@@ -436,13 +478,19 @@ extern "C" int fw_build_csr_device(const uint32_t *d_src, const uint32_t *d_dst,
     }
     const uint32_t G = (uint32_t)std::min<uint64_t>((uint64_t)sms * 4, (m + kTile - 1) / kTile);
     const uint64_t seg = ((m + G - 1) / G + kTile - 1) / kTile * kTile;  // whole tiles per CTA
+    // the input index rides along only when weights or labels must be gathered
+    const bool vals = d_w || d_lab;
+    v0 = v1 = nullptr;
     CUI(cudaMallocAsync(&k0, m * sizeof(uint64_t), st));
     CUI(cudaMallocAsync(&k1, m * sizeof(uint64_t), st));
-    CUI(cudaMallocAsync(&v0, m * sizeof(uint32_t), st));
-    CUI(cudaMallocAsync(&v1, m * sizeof(uint32_t), st));
+    if (vals) {
+        CUI(cudaMallocAsync(&v0, m * sizeof(uint32_t), st));
+        CUI(cudaMallocAsync(&v1, m * sizeof(uint32_t), st));
+    }
     CUI(cudaMallocAsync(&hist, (size_t)kRadix * G * sizeof(uint32_t), st));
     CUI(cudaMallocAsync(&dmax, sizeof(unsigned), st));
-    k_make_keys<<<sms * 8, 256, 0, st>>>(d_src, d_dst, m, bv, k0, v0);
+    const bool carried = d_w && !d_lab;
+    k_make_keys<<<sms * 8, 256, 0, st>>>(d_src, d_dst, m, bv, carried ? d_w : nullptr, k0, v0);
     for (int shift = 0; shift < nbits; shift += 8) {
         CUI(cudaMemsetAsync(dmax, 0, sizeof(unsigned), st));
         k_hist<<<G, kThreads, 0, st>>>(k0, m, seg, shift, hist);
@@ -451,17 +499,21 @@ extern "C" int fw_build_csr_device(const uint32_t *d_src, const uint32_t *d_dst,
         CUI(cudaMemcpyAsync(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost, st));
         CUI(cudaStreamSynchronize(st));
         if (h == m) continue;  // every key has the same digit: the pass is the identity
-        k_scatter<<<G, kThreads, 0, st>>>(k0, v0, m, seg, shift, hist, k1, v1);
+        if (vals)
+            k_scatter<true><<<G, kThreads, 0, st>>>(k0, v0, m, seg, shift, hist, k1, v1);
+        else
+            k_scatter<false><<<G, kThreads, 0, st>>>(k0, nullptr, m, seg, shift, hist, k1, nullptr);
         std::swap(k0, k1);
         std::swap(v0, v1);
     }
-    k_csr_edges<<<sms * 8, 256, 0, st>>>(k0, v0, m, bv, d_w, d_lab, d_tgt, d_w_out, d_lab_out);
+    k_csr_edges<<<sms * 8, 256, 0, st>>>(k0, v0, carried, m, bv, d_w, d_lab, d_tgt, d_w_out,
+                                         d_lab_out);
     k_csr_offsets<<<sms * 16, 256, 0, st>>>(k0, m, V, bv, d_off);
     CUI(cudaGetLastError());
     cudaFreeAsync(k0, st);
     cudaFreeAsync(k1, st);
-    cudaFreeAsync(v0, st);
-    cudaFreeAsync(v1, st);
+    if (v0) cudaFreeAsync(v0, st);
+    if (v1) cudaFreeAsync(v1, st);
     cudaFreeAsync(hist, st);
     cudaFreeAsync(dmax, st);
     CUI(cudaStreamSynchronize(st));

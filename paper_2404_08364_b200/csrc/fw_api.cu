@@ -538,10 +538,11 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
     // tree-order scans with certified accept tests; needs nonnegative finite
     // weights and sums far from overflow (cert_accept's bound)
     int mode = exact ? 1 : 0;
-    if (!exact && eng->order_mode == FW_ORDER_AUTO && app->weighted && !g->info.bad_weights) {
+    if (!exact && eng->order_mode == FW_ORDER_AUTO && !(app->weighted && g->info.bad_weights)) {
         double fmax = 1.0;
         if (app->app_id == FW_APP_NODE2VEC) fmax = std::max({1.0, app->inv_a, app->inv_b});
-        const double tot = (double)g->info.max_degree * fmax * (double)g->info.max_weight;
+        const double wmax = app->weighted ? (double)g->info.max_weight : 1.0;
+        const double tot = (double)g->info.max_degree * fmax * wmax;
         const char *env = getenv("FW_CERT");  // A/B override: 0 keeps the ordered kernels
         if (std::isfinite(fmax) && tot < 1e290 && !(env && env[0] == '0')) mode = 2;
     }

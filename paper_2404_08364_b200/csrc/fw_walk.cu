@@ -1423,15 +1423,19 @@ walk_kernel(const __grid_constant__ WalkArgs a) {
             bool have_u = false;
             if constexpr (SAMPLER == SAMPLER_DPRS) {
                 if constexpr (CERT) {
-                    // non-dyadic weights: weighted by construction (unweighted
-                    // sums are exact and run in mode 1)
+                    // sums that round: non-dyadic weights, or factors 1/a, 1/b
+                    // that are not powers of two (weighted or not)
                     if (APP == APP_NODE2VEC && s.prev >= 0) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
                             const bool win = (uint32_t)(s.phi - s.plo) <=
                                              a.merge_ratio * s.deg + 2 * kChunk;
-                            sel = a.fac32 ? (win ? dprs_n2v_pow2<true, true, true, false, true>(a, s, k, lane, woff)
-                                                 : dprs_n2v_pow2<true, true, false, false, true>(a, s, k, lane, woff))
-                                          : dprs_n2v_pow2<false, true, false, false, true>(a, s, k, lane, woff);
+                            if (a.weighted)
+                                sel = a.fac32 ? (win ? dprs_n2v_pow2<true, true, true, false, true>(a, s, k, lane, woff)
+                                                     : dprs_n2v_pow2<true, true, false, false, true>(a, s, k, lane, woff))
+                                              : dprs_n2v_pow2<false, true, false, false, true>(a, s, k, lane, woff);
+                            else
+                                sel = a.fac32 ? dprs_n2v_pow2<true, false, false, false, true>(a, s, k, lane, woff)
+                                              : dprs_n2v_pow2<false, false, false, false, true>(a, s, k, lane, woff);
                         } else {
                             sel = kCertFallback;
                         }

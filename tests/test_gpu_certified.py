@@ -81,6 +81,7 @@ def s16_lognormal():
     (dict(app="ppr", length=80, stop_prob=0.2), "auto"),
     (dict(app="metapath", length=5, schema=(0, 1, 2, 3, 4)), "auto"),
     (dict(app="node2vec", length=40, a=2.0, b=0.5), "zprs"),
+    (dict(app="node2vec", length=40, a=3.0, b=0.7, weighted=False), "auto"),
 ])
 def test_rmat_s16_lognormal_matches_oracle(s16_lognormal, app, sampler, slack):
     g = s16_lognormal
@@ -130,6 +131,20 @@ def test_zprs_hub_groups_certified(s16_lognormal):
             np.testing.assert_array_equal(ln, oln)
             np.testing.assert_array_equal(seq, oseq)
             assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()
+
+
+def test_unweighted_non_dyadic_factors_select_certified():
+    """Unweighted Node2Vec with a = 3, b = 0.7 on a weighted graph: 1/3 and
+    1/0.7 make the sums round, so DPRS runs certified (and ignores the
+    graph's weights, apps.py weighted=False)."""
+    g = rmat.rmat_graph(14)
+    starts = np.arange(g.vertex_count, dtype=np.int64)
+    app = dict(app="node2vec", length=40, a=3.0, b=0.7, weighted=False)
+    seq, ln, st = _run(g, starts, fw.AppConfig(**app), fw.EngineConfig(replay=True))
+    assert st.summation == "certified"
+    oseq, oln, ost = oracle.walk(g.offsets, g.targets, g.weights, g.labels, starts, **app)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq, oseq)
 
 
 def test_wide_lognormal_selects_certified_on_its_own():

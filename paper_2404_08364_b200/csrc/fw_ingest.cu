@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -525,6 +526,11 @@ extern "C" int fw_build_csr_device(const uint32_t *d_src, const uint32_t *d_dst,
 // targets u32[E], weights f32[E], [labels u8[E] if flags & 2], crc32 u32.
 // ---------------------------------------------------------------------------
 static const uint64_t kHeader = 21;
+// FWG1 streaming: reader threads x 2 pinned chunks, kept for the process
+static const uint64_t kFwg1Chunk = 16ull << 20;
+static const int kFwg1Threads = 8;
+static std::mutex g_pin_mu;
+static std::vector<void *> g_pin;
 
 extern "C" int fw_fwg1_info(const char *path, uint64_t *V, uint64_t *E, int32_t *flags) {
     if (!path || !V || !E || !flags) return set_err_ingest(FW_EVALIDATION, "null argument");
@@ -585,25 +591,32 @@ extern "C" int fw_fwg1_read(const char *path, uint64_t V, uint64_t E, int32_t fl
     const int fd = open(path, O_RDONLY);
     if (fd < 0) return set_err_ingest(FW_EFORMAT, "%s: cannot open", path);
     // Reader threads, each with its own stream and two pinned buffers: a
-    // thread reads chunk c (pread) while its previous chunk's H2D runs.
-    const uint64_t chunk = 32ull << 20;
-    const int nthreads = 4;
+    // thread reads chunk c (pread) while its previous chunk's H2D runs.  The
+    // pinned buffers are allocated once per process and reused (pinning 256
+    // MB per call cost more than the copies of a 2 GB file).
+    const uint64_t chunk = kFwg1Chunk;
+    const int nthreads = kFwg1Threads;
     int dev = 0;
     cudaGetDevice(&dev);
+    std::unique_lock<std::mutex> pin_lk(g_pin_mu);  // one FWG1 read at a time owns the pool
+    if (g_pin.empty()) {
+        g_pin.assign(2 * nthreads, nullptr);
+        for (auto &p : g_pin) {
+            if (cudaMallocHost(&p, chunk) != cudaSuccess) {
+                for (auto &q : g_pin)
+                    if (q) cudaFreeHost(q);
+                g_pin.clear();
+                return set_err_ingest(FW_ENOMEM, "pinned staging allocation failed");
+            }
+        }
+    }
     std::vector<int> trc(nthreads, FW_OK);
     std::vector<std::string> terr(nthreads);
     auto worker = [&](int tid) {
         cudaSetDevice(dev);
-        void *pin[2] = {nullptr, nullptr};
+        void *pin[2] = {g_pin[2 * tid], g_pin[2 * tid + 1]};
         cudaEvent_t ev[2];
         cudaStream_t ts;
-        if (cudaMallocHost(&pin[0], chunk) != cudaSuccess ||
-            cudaMallocHost(&pin[1], chunk) != cudaSuccess) {
-            trc[tid] = FW_ENOMEM;
-            terr[tid] = "pinned staging allocation failed";
-            if (pin[0]) cudaFreeHost(pin[0]);
-            return;
-        }
         cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking);
         cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
@@ -640,8 +653,6 @@ extern "C" int fw_fwg1_read(const char *path, uint64_t V, uint64_t E, int32_t fl
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
         cudaStreamDestroy(ts);
-        cudaFreeHost(pin[0]);
-        cudaFreeHost(pin[1]);
     };
     std::vector<std::thread> th;
     for (int t = 0; t < nthreads; t++) th.emplace_back(worker, t);

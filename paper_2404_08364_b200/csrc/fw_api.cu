@@ -281,20 +281,8 @@ static int graph_common_init(fw_graph *g, int device) {
     return FW_OK;
 }
 
-// Upload through a double-buffered pinned staging area.
-static int upload(void *dst, const void *src, size_t bytes, cudaStream_t st, void *pin[2],
-                  cudaEvent_t ev[2], size_t chunk) {
-    const char *s = (const char *)src;
-    char *d = (char *)dst;
-    int slot = 0;
-    for (size_t done = 0; done < bytes; done += chunk, slot ^= 1) {
-        const size_t n = std::min(chunk, bytes - done);
-        CU(cudaEventSynchronize(ev[slot]));
-        memcpy(pin[slot], s + done, n);
-        CU(cudaMemcpyAsync(d + done, pin[slot], n, cudaMemcpyHostToDevice, st));
-        CU(cudaEventRecord(ev[slot], st));
-    }
-    return FW_OK;
+namespace fwi {
+int staged_h2d(int n, const void *const *src, void *const *dst, const uint64_t *bytes);
 }
 
 extern "C" int fw_graph_create(const int64_t *offsets, const uint32_t *targets,
@@ -320,27 +308,13 @@ extern "C" int fw_graph_create(const int64_t *offsets, const uint32_t *targets,
         (e = cudaMalloc(&g->w, (E + 4) * sizeof(float))) != cudaSuccess ||        // 16-byte tiles
         (labels && (e = cudaMalloc(&g->lab, std::max<uint64_t>(E, 1))) != cudaSuccess))
         return fail(set_err(FW_ENOMEM, "graph allocation: %s", cudaGetErrorString(e)));
-    const size_t chunk = 64u << 20;
-    void *pin[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2];
-    cudaStream_t st;
-    if (cudaMallocHost(&pin[0], chunk) != cudaSuccess || cudaMallocHost(&pin[1], chunk) != cudaSuccess)
-        return fail(set_err(FW_ENOMEM, "pinned staging allocation failed"));
-    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
-    cudaEventRecord(ev[0], st);
-    cudaEventRecord(ev[1], st);
-    rc = upload(g->off, offsets, (V + 1) * sizeof(int64_t), st, pin, ev, chunk);
-    if (!rc && E) rc = upload(g->tgt, targets, E * sizeof(uint32_t), st, pin, ev, chunk);
-    if (!rc && E) rc = upload(g->w, weights, E * sizeof(float), st, pin, ev, chunk);
-    if (!rc && E && labels) rc = upload(g->lab, labels, E, st, pin, ev, chunk);
-    cudaStreamSynchronize(st);
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    cudaStreamDestroy(st);
-    cudaFreeHost(pin[0]);
-    cudaFreeHost(pin[1]);
+    {   // one pass through the process's pinned pool, 8 copy threads
+        const void *src[4] = {offsets, targets, weights, labels};
+        void *dst[4] = {g->off, g->tgt, g->w, g->lab};
+        const uint64_t bytes[4] = {(V + 1) * sizeof(int64_t), E * sizeof(uint32_t),
+                                   E * sizeof(float), labels ? E : 0};
+        rc = fwi::staged_h2d(4, src, dst, bytes);  // sets fw_last_error on failure
+    }
     if (rc) return fail(rc);
     if ((rc = profile_graph(g))) return fail(rc);
     *out = g;

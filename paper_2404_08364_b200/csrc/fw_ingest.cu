@@ -43,6 +43,7 @@
 namespace fwi {
 
 int set_err_ingest(int code, const char *fmt, ...);
+int staged_h2d(int n, const void *const *src, void *const *dst, const uint64_t *bytes);
 
 #define CUI(expr)                                                                          \
     do {                                                                                   \
@@ -555,6 +556,71 @@ extern "C" int fw_fwg1_info(const char *path, uint64_t *V, uint64_t *E, int32_t 
     *V = v;
     *E = e;
     *flags = f;
+    return FW_OK;
+}
+
+// Host arrays -> device arrays through the process's pinned pool: kFwg1Threads
+// threads, each memcpy-ing 16 MB chunks of the concatenated arrays into its two
+// pinned buffers while the previous chunk's H2D runs on its own stream
+// (fw_graph_create's upload: one thread and per-call pinned buffers moved
+// ~6 GB/s).
+int fwi::staged_h2d(int n, const void *const *src, void *const *dst, const uint64_t *bytes) {
+    uint64_t total = 0;
+    for (int i = 0; i < n; i++) total += bytes[i];
+    if (!total) return FW_OK;
+    const uint64_t chunk = kFwg1Chunk;
+    const int nthreads = kFwg1Threads;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::unique_lock<std::mutex> pin_lk(g_pin_mu);
+    if (g_pin.empty()) {
+        g_pin.assign(2 * nthreads, nullptr);
+        for (auto &p : g_pin) {
+            if (cudaMallocHost(&p, chunk) != cudaSuccess) {
+                for (auto &q : g_pin)
+                    if (q) cudaFreeHost(q);
+                g_pin.clear();
+                return set_err_ingest(FW_ENOMEM, "pinned staging allocation failed");
+            }
+        }
+    }
+    std::vector<int> trc(nthreads, FW_OK);
+    auto worker = [&](int tid) {
+        cudaSetDevice(dev);
+        void *pin[2] = {g_pin[2 * tid], g_pin[2 * tid + 1]};
+        cudaEvent_t ev[2];
+        cudaStream_t ts;
+        cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+        cudaEventRecord(ev[0], ts);
+        cudaEventRecord(ev[1], ts);
+        int slot = 0;
+        for (uint64_t c0 = (uint64_t)tid * chunk; c0 < total; c0 += (uint64_t)nthreads * chunk, slot ^= 1) {
+            const uint64_t cn = std::min(chunk, total - c0);
+            cudaEventSynchronize(ev[slot]);
+            uint64_t base = 0;
+            for (int i = 0; i < n; i++) {  // the chunk's intersection with each array
+                const uint64_t lo = std::max(c0, base), hi = std::min(c0 + cn, base + bytes[i]);
+                if (lo < hi) {
+                    memcpy((char *)pin[slot] + (lo - c0), (const char *)src[i] + (lo - base), hi - lo);
+                    cudaMemcpyAsync((char *)dst[i] + (lo - base), (char *)pin[slot] + (lo - c0),
+                                    hi - lo, cudaMemcpyHostToDevice, ts);
+                }
+                base += bytes[i];
+            }
+            cudaEventRecord(ev[slot], ts);
+        }
+        if (cudaStreamSynchronize(ts) != cudaSuccess) trc[tid] = FW_ECUDA;
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        cudaStreamDestroy(ts);
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; t++) th.emplace_back(worker, t);
+    for (auto &t : th) t.join();
+    for (int t = 0; t < nthreads; t++)
+        if (trc[t]) return set_err_ingest(trc[t], "host-to-device upload failed");
     return FW_OK;
 }
 

@@ -489,8 +489,12 @@ def bench_ours(args):
             dist.barrier()
         t0 = time.perf_counter()
         e2e_sampled = 0
+        call_ms, dev_ms = [], []
         for _ in range(e2e_iters):
+            tc = time.perf_counter()
             host_call()
+            call_ms.append(1e3 * (time.perf_counter() - tc))
+            dev_ms.append(fst.total_ms)
             e2e_sampled += fst.sampled_steps
         e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=cdev)
         e2e_tot = torch.tensor([e2e_sampled], dtype=torch.int64, device=cdev)
@@ -500,6 +504,8 @@ def bench_ours(args):
         e2e = {"value": int(e2e_tot.item()) / float(e2e_s.item()), "unit": "steps/s",
                "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * L * 4 + n * 4,
                "path": "fw_walk (C ABI, pinned host buffers)", "iters": e2e_iters,
+               "call_ms_median": statistics.median(call_ms),
+               "device_ms_median": statistics.median(dev_ms),
                "d2h_pieces_overlapped": int(fst.d2h_pieces)}
         summation = {0: "sequential", 1: "exact", 2: "certified"}.get(int(fst.exact_order))
         del hseq

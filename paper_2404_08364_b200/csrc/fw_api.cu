@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -675,6 +676,15 @@ constexpr uint64_t kD2hMinQueries = 65536;  // below this, copy after the walk
 extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t base_qid,
                        const fw_app *app, const fw_engine *eng, uint64_t seed,
                        uint32_t *out_seq, uint32_t *out_len, fw_stats *stats) {
+    static const bool trace = [] {
+        const char *e = getenv("FW_HOST_TRACE");
+        return e && e[0] == '1';
+    }();
+    const auto t_in = std::chrono::steady_clock::now();
+    auto us = [&]() {
+        return (long)std::chrono::duration_cast<std::chrono::microseconds>(
+                   std::chrono::steady_clock::now() - t_in).count();
+    };
     int rc = check_cfg(g, app, eng);
     if (rc) return rc;
     CU(cudaSetDevice(g->device));
@@ -686,11 +696,17 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
     // device memory); each buffer's D2H overlaps the next sub-launch.
     const uint64_t per_q = L * sizeof(uint32_t) + sizeof(uint32_t) + sizeof(int64_t);
     uint64_t limit = g->scratch_limit;
-    if (!limit) {
+    uint64_t held = 0;
+    for (int i = 0; i < 2; i++) held += g->starts[i].cap + g->seq[i].cap + g->len[i].cap;
+    const bool fits0 = g->starts[0].cap >= n * sizeof(int64_t) &&
+                       g->seq[0].cap >= n * L * sizeof(uint32_t) &&
+                       g->len[0].cap >= n * sizeof(uint32_t);
+    if (!limit && fits0) {
+        limit = std::max(held, n * per_q);  // one launch in the staging already held
+    } else if (!limit) {
+        // cudaMemGetInfo costs ~0.5 ms: asked only when the staging must grow
         size_t fr = 0, tot = 0;
         CU(cudaMemGetInfo(&fr, &tot));
-        uint64_t held = 0;
-        for (int i = 0; i < 2; i++) held += g->starts[i].cap + g->seq[i].cap + g->len[i].cap;
         limit = (uint64_t)((double)(fr + held) * 0.9);
     }
     const uint64_t rows_cap = std::max<uint64_t>(limit / per_q, 2);
@@ -791,6 +807,7 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         }
         cudaEventRecord(e3, st);
     }
+    const long t_issued = us();
     // always drain both streams: no copy may still target the caller's buffers
     cudaError_t ce = cudaStreamSynchronize(st);
     const cudaError_t ce2 = cudaStreamSynchronize(cs);
@@ -822,6 +839,9 @@ extern "C" int fw_walk(fw_graph *g, const int64_t *starts, uint64_t n, uint64_t 
         for (int i = 0; i < 2; i++) sb += g->starts[i].cap + g->seq[i].cap + g->len[i].cap;
         stats->scratch_bytes = sb;
     }
+    if (trace)
+        fprintf(stderr, "fw_walk host: issued %ld us, returned %ld us (n=%llu)\n", t_issued, us(),
+                (unsigned long long)n);
     return rc;
 }
 

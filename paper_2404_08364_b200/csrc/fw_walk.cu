@@ -1554,11 +1554,15 @@ static cudaError_t launch_t(const WalkArgs &a, int grid, cudaStream_t stream) {
 
 template <int APP, int SAMPLER, int MODE>
 static int occupancy_t() {
-    int nb = 0;
-    cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, MODE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, walk_smem_bytes(APP));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_kernel<APP, SAMPLER, MODE>,
-                                                  kWalkThreads, walk_smem_bytes(APP));
+    // per kernel and process (the same on every B200; queried once, not per launch)
+    static const int nb = [] {
+        int b = 0;
+        cudaFuncSetAttribute(walk_kernel<APP, SAMPLER, MODE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, walk_smem_bytes(APP));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, walk_kernel<APP, SAMPLER, MODE>,
+                                                      kWalkThreads, walk_smem_bytes(APP));
+        return b;
+    }();
     return nb;
 }
 

@@ -181,3 +181,26 @@ def test_device_crc32_equals_zlib(n, shift):
     _lib.check(_lib.load().fw_crc32_device(d.data_ptr() + shift if n else None, n,
                                            ctypes.byref(out), None))
     assert out.value == zlib.crc32(host[shift:].tobytes()) & 0xFFFFFFFF
+
+
+@pytest.mark.parametrize("with_w", [True, False])
+def test_build_csr_device_without_labels(with_w):
+    """The sort's value variants: weights without labels ride through the sort
+    as the value (no gather), and with neither only the keys move (weights 1)."""
+    import torch
+    rs = np.random.default_rng(11)
+    V, m = 1 << 16, 1 << 21
+    src = rs.integers(0, V, m).astype(np.uint32)
+    dst = rs.integers(0, V, m).astype(np.uint32)
+    w = rs.random(m).astype(np.float32)
+    d = torch.device("cuda", 0)
+    t = (torch.from_numpy(src.view(np.int32)).to(d), torch.from_numpy(dst.view(np.int32)).to(d),
+         torch.from_numpy(w).to(d) if with_w else None, None)
+    dg = fw.build_csr_device(t, V)
+    want = oracle.ingest.build_csr(src, dst, w if with_w else np.ones(m, np.float32),
+                                   np.zeros(m, np.uint8), V)
+    np.testing.assert_array_equal(dg.offsets.cpu().numpy(), want[0])
+    np.testing.assert_array_equal(dg.targets.cpu().numpy().view(np.uint32), want[1])
+    np.testing.assert_array_equal(dg.weights.cpu().numpy(), want[2])
+    assert dg.labels is None
+    dg.close()

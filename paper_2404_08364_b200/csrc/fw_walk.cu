@@ -378,7 +378,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
     const uint32_t deg = s.deg;
     const uint32_t nl = k < deg ? k : deg;
     // app weights are exactly representable as float except for node2vec
-    const bool staged = APP != APP_NODE2VEC && deg <= kHashSlots;
+    const bool staged = APP != APP_NODE2VEC && deg <= warp_slots(APP);
     float *stage = reinterpret_cast<float *>(fw_smem) + woff;
     if (nl <= 32) {  // one group: physical lane == logical lane
         const uint32_t j = lane;
@@ -392,7 +392,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
             // lane j keeps only its nonzero elements, compacted in chunk
             // order into its own staging slots j + k*m (m <= chunk index, so
             // the list never outruns the dense layout), chunk ids alongside.
-            uint16_t *cst = reinterpret_cast<uint16_t *>(fw_smem + woff + kHashSlots);
+            uint16_t *cst = reinterpret_cast<uint16_t *>(fw_smem + woff + warp_slots(APP));
             uint32_t m = 0;
             if (j < nl) {
                 uint32_t c = 0, i = j;
@@ -448,7 +448,7 @@ __device__ uint32_t zprs_warp(const WalkArgs &a, const StepCtx &s, uint32_t k, i
         return m ? c : 0;
     }
     if (nl <= 256) {  // up to 8 groups: lane sums -> exclusive prefixes in smem
-        double *E = reinterpret_cast<double *>(fw_smem + woff + kHashSlots);
+        double *E = reinterpret_cast<double *>(fw_smem + woff + warp_slots(APP));
         const uint32_t ng = (nl + 31) >> 5;
         double ecarry = 0.0;
         for (uint32_t g = 0; g < ng; g++) {

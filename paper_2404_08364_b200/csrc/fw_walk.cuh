@@ -17,7 +17,12 @@ constexpr int kWalkThreads = FW_WALK_THREADS;  // 4 warp walkers per CTA
 #ifndef FW_MIN_BLOCKS_N2V
 #define FW_MIN_BLOCKS_N2V 7
 #endif
-constexpr int walk_min_blocks(int app) { return app == 2 ? FW_MIN_BLOCKS_N2V : FW_MIN_BLOCKS; }
+#ifndef FW_MIN_BLOCKS_MP
+#define FW_MIN_BLOCKS_MP FW_MIN_BLOCKS
+#endif
+constexpr int walk_min_blocks(int app) {
+    return app == 2 ? FW_MIN_BLOCKS_N2V : app == 3 ? FW_MIN_BLOCKS_MP : FW_MIN_BLOCKS;
+}
 // Per-warp shared memory (32-bit words):
 //   [0, slots)            first-order apps: ZPRS weight staging (kHashSlots);
 //                         node2vec: the N(prev) window table (kTabSlots)
@@ -28,7 +33,14 @@ constexpr int walk_min_blocks(int app) { return app == 2 ? FW_MIN_BLOCKS_N2V : F
 constexpr uint32_t kHashSlots = 1024;
 constexpr uint32_t kTabSlots = 1472;
 constexpr uint32_t kChunk = 256;  // N(prev) entries per table window
-__host__ __device__ constexpr uint32_t warp_slots(int app) { return app == 2 ? kTabSlots : kHashSlots; }
+#ifndef FW_MP_SLOTS
+#define FW_MP_SLOTS 1024
+#endif
+constexpr uint32_t kMpSlots = FW_MP_SLOTS;  // MetaPath staging (occupancy trade)
+static_assert(kMpSlots <= kHashSlots, "MetaPath staging is at most the first-order size");
+__host__ __device__ constexpr uint32_t warp_slots(int app) {
+    return app == 2 ? kTabSlots : app == 3 ? kMpSlots : kHashSlots;
+}
 __host__ __device__ constexpr uint32_t stats_word(int app) { return warp_slots(app) + 2 * 256; }
 __host__ __device__ constexpr uint32_t ctl_word(int app) { return stats_word(app) + 2 * 8; }
 __host__ __device__ constexpr uint32_t warp_words(int app) { return ctl_word(app) + 8; }

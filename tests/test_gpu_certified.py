@@ -159,3 +159,29 @@ def test_wide_lognormal_selects_certified_on_its_own():
     np.testing.assert_array_equal(ln, oln)
     np.testing.assert_array_equal(seq, oseq)
     assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()
+
+
+def _golden_names():
+    from conftest import Golden
+    return sorted(Golden().cases)
+
+
+@pytest.mark.parametrize("name", _golden_names())
+def test_every_golden_case_in_certified_mode(golden, name):
+    """Mode 2 forced on all 27 reference goldens: odd and tiny lane widths
+    (k = 3..1000, which take the in-order re-run), d_t variants, stars, PPR
+    and MetaPath, unweighted runs, the 2^63+5 seed."""
+    case = golden.cases[name]
+    off, tgt, w, lab = golden.graph(case["graph"])
+    g = fw.Graph(len(off) - 1, len(tgt), off, tgt, w, lab)
+    app = dict(case["app"])
+    if "schema" in app:
+        app["schema"] = tuple(app["schema"])
+    eng = fw.EngineConfig(replay=True, **case["eng"])
+    with _env(FW_FORCE_CERT="1"):
+        seq, ln, st = _run(g, golden.starts(name), fw.AppConfig(**app), eng, case["seed"])
+    want_seq, want_len, want_stats = golden.expected(name)
+    assert st.summation == "certified"
+    np.testing.assert_array_equal(ln, want_len)
+    np.testing.assert_array_equal(seq, want_seq)
+    assert [getattr(st, f) for f in STAT_NAMES] == want_stats.tolist()

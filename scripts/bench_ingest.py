@@ -1,7 +1,8 @@
 """Graph-ingest timing on one B200: the device
 build_csr (fw_build_csr_device: stable LSD radix sort, lexsort semantics of
-reswalk graph.py:138-169) and the FWG1 load (fw_fwg1_read: pinned double
-buffers + device CRC-32, graph.py:225-254), at R-MAT scale 22 and 24.
+reswalk graph.py:138-169), the FWG1 load (fw_fwg1_read: 8 reader threads,
+pinned double buffers, device CRC-32, graph.py:225-254) and fw_graph_create
+from host arrays, at R-MAT scale 22 and 24.
 
 Prints one JSON object per measurement.  The CPU column restates
 build_csr's own numpy call (np.lexsort((dst, src)) + bincount) on the same
@@ -100,11 +101,8 @@ def main():
                               "equal_to_device": bool(ok)}), flush=True)
             del hs, hd, targets, order
         # FWG1: write once from the host, then stream it back to the device
-        dg = graph.DeviceGraph(V, E, off, tgt, w_out, None, device=0) \
-            if hasattr(graph, "DeviceGraph") else None
-        if dg is None:
-            from paper_2404_08364_b200.engine import DeviceGraph
-            dg = DeviceGraph(V, E, off, tgt, w_out, None, device=0)
+        from paper_2404_08364_b200.engine import DeviceGraph
+        dg = DeviceGraph(V, E, off, tgt, w_out, None, device=0)
         path = os.path.join(args.fwg1_dir, f"rmat{s}.fwg")
         hg = dg.to_host()
         graph.save_binary(hg, path)

@@ -105,6 +105,23 @@ def workload_name(args, app):
     return f"{metric_name(args).split()[0]}{extra} length {app.length}, {q}, R-MAT scale-{args.scale} ef16{wt}"
 
 
+def workload_config(args, app, world):
+    """The workload-defining `config` object, identical for both arms (the
+    measurement outputs of a run go under "run")."""
+    V = 1 << args.scale
+    n_total = args.nq if args.nq else (V if args.scale < 26 else 1 << 24)
+    if args.scaling == "strong":
+        per_gpu = n_total // world  # rank 0's share (dist.partition)
+        total = n_total
+    else:
+        per_gpu, total = n_total, n_total * world
+    return {"workload": workload_name(args, app), "graph": f"rmat-s{args.scale}-ef16",
+            "sampler": args.sampler, "weights": args.weights, "vertices": V,
+            "csr_entries": 16 * V, "queries_per_gpu": per_gpu, "total_queries": total,
+            "parallelism": f"replicated graph, qids partitioned x{world}",
+            "l2": "inputs larger than L2 (graph + result pool > 126 MB), no flush"}
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -300,9 +317,9 @@ def bench_reference(args):
         "impl": "reference", "metric": metric_name(args), "value": value, "unit": "steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * tot_t / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp64+u64", "data": "synthetic",
-        "config": {"workload": workload_name(args, app), "graph": f"rmat-s{args.scale}-ef16", "sampler": args.sampler,
-                   "sample_queries_per_step": n},
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "fp64+u64", "data": "synthetic",
+        "config": workload_config(args, app, int(os.environ.get("WORLD_SIZE", "1"))),
+        "sample_queries_per_step": n,
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": kind,
                          "sample": f"{n} queries per step, replay mode, workers={cores}"},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
@@ -550,19 +567,14 @@ def bench_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "fp64+u64", "data": "synthetic",
-            "config": {"workload": workload, "graph": f"rmat-s{args.scale}-ef16", "sampler": args.sampler,
-                       "vertices": V, "csr_entries": E_, "queries_per_gpu": n,
-                       "replicate_s": None if world == 1 else round(t_rep, 3),
-                       "gather_ms": gather_ms,
-                       "gather_bytes": (n_total * L * 4 + n_total * 4) if gather_ms else None,
-                       "per_rank_walk_ms": [round(x, 3) for x in per_rank_ms],
-                       "total_queries": n_total if args.scaling == "strong" else n_total * world,
-                       "backend": backend if world > 1 else None,
-                       "parallelism": f"replicated graph, qids partitioned x{world}",
-                       "l2": "inputs larger than L2 (graph + result pool > 126 MB), no flush",
-                       "weights": args.weights, "summation": summation,
-                       "sampled_steps_per_gpu_step": sampled // args.steps,
-                       "walk_attempts_per_step": int(st[0]) // args.steps},
+            "config": workload_config(args, app, world),
+            "run": {"replicate_s": None if world == 1 else round(t_rep, 3),
+                    "gather_ms": gather_ms,
+                    "gather_bytes": (n_total * L * 4 + n_total * 4) if gather_ms else None,
+                    "per_rank_walk_ms": [round(x, 3) for x in per_rank_ms],
+                    "backend": backend if world > 1 else None, "summation": summation,
+                    "sampled_steps_per_gpu_step": sampled // args.steps,
+                    "walk_attempts_per_step": int(st[0]) // args.steps},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps, "load_imbalance_tail": tail,
             "clocks": clk,

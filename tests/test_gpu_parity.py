@@ -205,7 +205,7 @@ def test_torchrun_two_ranks_strong_scaling_gather(tmp_path):
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert line["config"]["queries_per_gpu"] == n // 2
-    assert line["config"]["gather_ms"] is not None and len(line["config"]["per_rank_walk_ms"]) == 2
+    assert line["run"]["gather_ms"] is not None and len(line["run"]["per_rank_walk_ms"]) == 2
     z = np.load(out)
     g = rmat.rmat_graph(14, labels=False)
     starts = np.arange(n, dtype=np.int64) % g.vertex_count

@@ -579,12 +579,35 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         // an integer multiple of 2^G, so w * 2^-G is an exact integer; a
         // lane's 4 of them must fit a u32 and the scaled prefilter bound
         // must stay finite
-        const double sc = std::ldexp(1.0, (int)-G);
+        double sc = std::ldexp(1.0, (int)-G);
         const char *env = getenv("FW_ISCAN");  // A/B override: 0 forces the fp64 tile scan
+        const bool iscan_ok = !(env && env[0] == '0');
+        bool qscan = false;
+        if (mode == 2 && a.fac32 && app->weighted && app->app_id == FW_APP_NODE2VEC &&
+            g->info.max_weight > 0.0f && iscan_ok) {
+            // certified mode: quantized integer tile sums.  Scale 2^s so every
+            // scaled app weight is < 2^29 (a lane's 4 fit a u32); the scaled
+            // products stay exact in fp32 (power-of-two factors, no underflow)
+            const double xm = std::max({1.0, app->inv_a, app->inv_b}) * (double)g->info.max_weight;
+            int e2 = 0;
+            std::frexp(xm, &e2);  // xm < 2^e2
+            const int sh = 29 - e2;
+            int ka = 0, kb = 0;
+            std::frexp(app->inv_a, &ka);
+            std::frexp(app->inv_b, &kb);
+            const int kmin = std::min({0, ka - 1, kb - 1});
+            if (sh >= -100 && sh <= 100 &&
+                (long)g->info.min_weight_lowbit_exp + kmin + sh >= -149) {
+                sc = std::ldexp(1.0, sh);
+                xmax = xm;
+                qscan = true;
+            }
+        }
         const double ws = (double)a.accept_wmax * sc;  // the kernel's prefilter has no disable
-        a.iscan = exact && a.fac32 && G >= -126 && G <= 126 && 4.0 * xmax * sc < 2147483648.0 &&
+        a.iscan = ((exact && G >= -126 && G <= 126) || qscan) && a.fac32 &&
+                  4.0 * xmax * sc < 2147483648.0 &&
                   std::max({1.0, app->inv_a, app->inv_b}) * sc <= 1e37 && std::isfinite(ws) &&
-                  ws <= 1e37 && !(env && env[0] == '0') ? 1 : 0;
+                  ws <= 1e37 && iscan_ok ? 1 : 0;
         a.iscale = a.iscan ? (float)sc : 1.0f;
         a.accept_wmax_s = a.iscan ? (float)ws : INFINITY;
         a.fa32 = a.inv_a32 * a.iscale;  // powers of two: exact

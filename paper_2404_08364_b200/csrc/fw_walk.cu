@@ -110,8 +110,8 @@ __device__ __forceinline__ uint32_t accept_thr(float wmax, double base) {
 // and otherwise (probability ~ i * 2^-50) the step is ambiguous and is
 // re-run on the ordered path.  Returns 1 accept, 0 reject, 2 ambiguous.
 __device__ __forceinline__ int cert_accept(double r, double P, double w, double tot, uint32_t i,
-                                           double slack) {
-    const double d = __dmul_ru(tot, __dmul_ru((double)i + 160.0, slack));
+                                           double slack, double abs_err = 0.0) {
+    const double d = __dadd_ru(__dmul_ru(tot, __dmul_ru((double)i + 160.0, slack)), abs_err);
     if (__dmul_ru(r, __dadd_ru(P, d)) < w) return 1;
     if (__dmul_rd(r, fmax(__dadd_rd(P, -d), 0.0)) >= w) return 0;
     return 2;
@@ -1098,9 +1098,18 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             // fl(r * P') < w' in units of 2^G is the reference's test).
             uint32_t wi[4];
 #pragma unroll
-            for (int e = 0; e < 4; e++) wi[e] = __float2uint_rz(wp[e]);  // factors carry 2^-G
+            for (int e = 0; e < 4; e++) {
+                // exact: the factors carry 2^-G and every product is an integer.
+                // CERT (sums that round): the factors carry a scale 2^s with
+                // every product < 2^29; wi is its nearest integer, so the
+                // integer prefix is within 0.5 per element of the exact one
+                // (cert_accept's abs_err) while the tested w stays exact
+                wi[e] = CERT ? __float2uint_rn(wp[e]) : __float2uint_rz(wp[e]);
+            }
             const uint32_t li = (wi[0] + wi[1]) + (wi[2] + wi[3]);
-            const uint32_t thr = accept_thr_raw(a.accept_wmax_s, (float)icarry);
+            const uint32_t thr =
+                CERT ? accept_thr_f(fmaxf(fmaxf(wp[0], wp[1]), fmaxf(wp[2], wp[3])), (float)icarry)
+                     : accept_thr_raw(a.accept_wmax_s, (float)icarry);
             const uint32_t slo = __reduce_add_sync(FULL, li & 0xFFFFu);
             const uint32_t shi = __reduce_add_sync(FULL, li >> 16);
             const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
@@ -1120,13 +1129,26 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                 const double incl = warp_incl_scan_p(l3);
                 double run = __dadd_rn((double)icarry, __dadd_rn(incl, -l3));  // exact
                 if (ymin <= thr) {
+                    [[maybe_unused]] const double tot =
+                        (double)(icarry + ((uint64_t)shi << 16) + slo) + 64.0;
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
-                        const double w = (double)wi[e];
-                        run = __dadd_rn(run, w);
+                        run = __dadd_rn(run, (double)wi[e]);
                         if (y[e] <= thr) {
                             const double r = u01_word(wd[e]);
-                            if (w > 0.0 && __dmul_rn(r, run) < w) cand = (uint32_t)(i0 + e) + 1;
+                            if constexpr (CERT) {
+                                const double w = (double)wp[e];  // exact, scaled
+                                if (w > 0.0) {
+                                    const uint32_t ie = (uint32_t)(i0 + e);
+                                    const int c_ = cert_accept(r, run, w, tot, ie, a.cert_slack,
+                                                               0.5 * (double)(ie + 1));
+                                    if (c_ == 1) cand = ie + 1;
+                                    else if (c_ == 2) amb = ie + 1;
+                                }
+                            } else {
+                                const double w = (double)wi[e];
+                                if (w > 0.0 && __dmul_rn(r, run) < w) cand = (uint32_t)(i0 + e) + 1;
+                            }
                         }
                     }
                 }
@@ -1429,7 +1451,10 @@ walk_kernel(const __grid_constant__ WalkArgs a) {
                         if (k >= 4 && k <= 256 && (k & (k - 1)) == 0) {
                             const bool win = (uint32_t)(s.phi - s.plo) <=
                                              a.merge_ratio * s.deg + 2 * kChunk;
-                            if (a.weighted)
+                            if (a.weighted && a.iscan)  // quantized integer tile sums
+                                sel = win ? dprs_n2v_pow2<true, true, true, true, true>(a, s, k, lane, woff)
+                                          : dprs_n2v_pow2<true, true, false, true, true>(a, s, k, lane, woff);
+                            else if (a.weighted)
                                 sel = a.fac32 ? (win ? dprs_n2v_pow2<true, true, true, false, true>(a, s, k, lane, woff)
                                                      : dprs_n2v_pow2<true, true, false, false, true>(a, s, k, lane, woff))
                                               : dprs_n2v_pow2<false, true, false, false, true>(a, s, k, lane, woff);

@@ -583,6 +583,20 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
         const char *env = getenv("FW_ISCAN");  // A/B override: 0 forces the fp64 tile scan
         const bool iscan_ok = !(env && env[0] == '0');
         bool qscan = false;
+        a.qscale = 1.0;
+        if (mode == 2 && !a.fac32 && app->weighted && app->app_id == FW_APP_NODE2VEC &&
+            g->info.max_weight > 0.0f && iscan_ok) {
+            // fp64 factors (1/a, 1/b not powers of two): scale the fp64
+            // products f * w by 2^s < 2^29 / max; exact in fp64, then rounded
+            const double xm = std::max({1.0, app->inv_a, app->inv_b}) * (double)g->info.max_weight;
+            int e2 = 0;
+            std::frexp(xm, &e2);
+            const int sh = 29 - e2;
+            if (sh >= -900 && sh <= 900 && std::isfinite(xm)) {
+                a.qscale = std::ldexp(1.0, sh);
+                a.iscan = 1;  // selects the quantized tile sums for fp64 factors
+            }
+        }
         if (mode == 2 && a.fac32 && app->weighted && app->app_id == FW_APP_NODE2VEC &&
             g->info.max_weight > 0.0f && iscan_ok) {
             // certified mode: quantized integer tile sums.  Scale 2^s so every
@@ -604,10 +618,11 @@ static int launch(fw_graph *g, const int64_t *d_starts, uint64_t n, uint64_t bas
             }
         }
         const double ws = (double)a.accept_wmax * sc;  // the kernel's prefilter has no disable
-        a.iscan = ((exact && G >= -126 && G <= 126) || qscan) && a.fac32 &&
+        const bool q64 = a.iscan == 1;  // set just above: fp64-factor quantized sums
+        a.iscan = q64 || (((exact && G >= -126 && G <= 126) || qscan) && a.fac32 &&
                   4.0 * xmax * sc < 2147483648.0 &&
                   std::max({1.0, app->inv_a, app->inv_b}) * sc <= 1e37 && std::isfinite(ws) &&
-                  ws <= 1e37 && iscan_ok ? 1 : 0;
+                  ws <= 1e37 && iscan_ok) ? 1 : 0;
         a.iscale = a.iscan ? (float)sc : 1.0f;
         a.accept_wmax_s = a.iscan ? (float)ws : INFINITY;
         a.fa32 = a.inv_a32 * a.iscale;  // powers of two: exact

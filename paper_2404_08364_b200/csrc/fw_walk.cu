@@ -1097,19 +1097,32 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             // (a scale by a power of two commutes with fp64 rounding, so
             // fl(r * P') < w' in units of 2^G is the reference's test).
             uint32_t wi[4];
+            [[maybe_unused]] double wqv[4];  // !F32 (CERT only): exact fp64 products, scaled
 #pragma unroll
             for (int e = 0; e < 4; e++) {
                 // exact: the factors carry 2^-G and every product is an integer.
-                // CERT (sums that round): the factors carry a scale 2^s with
-                // every product < 2^29; wi is its nearest integer, so the
-                // integer prefix is within 0.5 per element of the exact one
+                // CERT (sums that round): the products carry a scale 2^s that
+                // keeps them < 2^29; wi is the nearest integer, so the integer
+                // prefix is within 0.5 per element of the exact one
                 // (cert_accept's abs_err) while the tested w stays exact
-                wi[e] = CERT ? __float2uint_rn(wp[e]) : __float2uint_rz(wp[e]);
+                if constexpr (F32) {
+                    wi[e] = CERT ? __float2uint_rn(wp[e]) : __float2uint_rz(wp[e]);
+                } else {
+                    const double f = u[e] == prev ? a.inv_a : (((mem >> e) & 1) ? 1.0 : a.inv_b);
+                    wqv[e] = __dmul_rn(__dmul_rn(f, (double)wf[e]), a.qscale);  // power of two: exact
+                    wi[e] = __double2uint_rn(wqv[e]);
+                }
             }
             const uint32_t li = (wi[0] + wi[1]) + (wi[2] + wi[3]);
-            const uint32_t thr =
-                CERT ? accept_thr_f(fmaxf(fmaxf(wp[0], wp[1]), fmaxf(wp[2], wp[3])), (float)icarry)
-                     : accept_thr_raw(a.accept_wmax_s, (float)icarry);
+            uint32_t thr;
+            if constexpr (!CERT) {
+                thr = accept_thr_raw(a.accept_wmax_s, (float)icarry);
+            } else if constexpr (F32) {
+                thr = accept_thr_f(fmaxf(fmaxf(wp[0], wp[1]), fmaxf(wp[2], wp[3])), (float)icarry);
+            } else {
+                thr = accept_thr_f(__double2float_ru(fmax(fmax(wqv[0], wqv[1]), fmax(wqv[2], wqv[3]))),
+                                   (float)icarry);
+            }
             const uint32_t slo = __reduce_add_sync(FULL, li & 0xFFFFu);
             const uint32_t shi = __reduce_add_sync(FULL, li >> 16);
             const uint4 qa = *reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(fw_smem) + wq);
@@ -1137,7 +1150,7 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
                         if (y[e] <= thr) {
                             const double r = u01_word(wd[e]);
                             if constexpr (CERT) {
-                                const double w = (double)wp[e];  // exact, scaled
+                                const double w = F32 ? (double)wp[e] : wqv[e];  // exact, scaled
                                 if (w > 0.0) {
                                     const uint32_t ie = (uint32_t)(i0 + e);
                                     const int c_ = cert_accept(r, run, w, tot, ie, a.cert_slack,
@@ -1452,8 +1465,9 @@ walk_kernel(const __grid_constant__ WalkArgs a) {
                             const bool win = (uint32_t)(s.phi - s.plo) <=
                                              a.merge_ratio * s.deg + 2 * kChunk;
                             if (a.weighted && a.iscan)  // quantized integer tile sums
-                                sel = win ? dprs_n2v_pow2<true, true, true, true, true>(a, s, k, lane, woff)
-                                          : dprs_n2v_pow2<true, true, false, true, true>(a, s, k, lane, woff);
+                                sel = !a.fac32 ? dprs_n2v_pow2<false, true, false, true, true>(a, s, k, lane, woff)
+                                      : win    ? dprs_n2v_pow2<true, true, true, true, true>(a, s, k, lane, woff)
+                                               : dprs_n2v_pow2<true, true, false, true, true>(a, s, k, lane, woff);
                             else if (a.weighted)
                                 sel = a.fac32 ? (win ? dprs_n2v_pow2<true, true, true, false, true>(a, s, k, lane, woff)
                                                      : dprs_n2v_pow2<true, true, false, false, true>(a, s, k, lane, woff))

@@ -88,6 +88,9 @@ struct WalkArgs {
     // mode 2: certified accept tests; slack = 2^-50 (FW_CERT_SLACK scales it
     // up in tests to force the ordered re-run)
     double cert_slack;
+    // mode 2, fp64 factors: the power-of-two scale of the quantized integer
+    // tile sums (the fp32-factor path folds it into fa32/f132/fb32)
+    double qscale;
     unsigned long long *queue;
     long long *stats;  // ST_COUNT counters (accumulated)
 };

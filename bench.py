@@ -74,10 +74,14 @@ def parse_args():
     p.add_argument("--scaling", choices=["weak", "strong"], default="strong",
                    help="strong: one query set partitioned over the GPUs (default); "
                         "weak: every GPU walks its own full query set (disjoint global qids)")
-    p.add_argument("--no-gather", action="store_true",
-                   help="N>1 strong scaling: skip the (separately timed) gather to rank 0")
+    p.add_argument("--gather", choices=["direct", "nccl", "none"], default="direct",
+                   help="N>1 strong scaling: how the paths reach rank 0. direct: every rank's "
+                        "walk kernel stores its rows straight into rank 0's buffer (CUDA IPC, "
+                        "NVLink peer stores, no gather phase); nccl: point-to-point NCCL "
+                        "send/recv after the walk, timed separately; none")
+    p.add_argument("--no-gather", action="store_true", help="same as --gather none")
     p.add_argument("--dump-gather", default=None,
-                   help="with --gather: rank 0 saves the gathered paths (.npz) for tests")
+                   help="N>1: rank 0 saves the gathered paths (.npz) for tests")
     return p.parse_args()
 
 
@@ -407,8 +411,23 @@ def bench_ours(args):
                 else make_starts(args, V, hub)[:n])
     starts = torch.from_numpy(np.ascontiguousarray(starts_h)).to(dev)
     L = app.length
-    seq = torch.empty(n * L, dtype=torch.int32, device=dev)
-    lens = torch.empty(n, dtype=torch.int32, device=dev)
+    gather = ("none" if (args.no_gather or world == 1 or args.scaling != "strong")
+              else args.gather)
+    shared = None
+    if gather == "direct":
+        # rank 0's result buffers, exported by CUDA IPC: each rank's kernel
+        # writes its qid range's rows straight into them (fused gather)
+        own = None
+        if rank == 0:
+            own = [torch.empty(n_total * L, dtype=torch.int32, device=dev),
+                   torch.empty(n_total, dtype=torch.int32, device=dev)]
+        shared = fwd.share_buffers(own, src=0)
+        seq_ptr = shared[0].data_ptr() + lo * L * 4
+        len_ptr = shared[1].data_ptr() + lo * 4
+    else:
+        seq = torch.empty(n * L, dtype=torch.int32, device=dev)
+        lens = torch.empty(n, dtype=torch.int32, device=dev)
+        seq_ptr, len_ptr = seq.data_ptr(), lens.data_ptr()
     stats = torch.zeros(10, dtype=torch.int64, device=dev)
     a_s, e_s, _schema = _fw_structs(app, fw.EngineConfig(replay=True, sampler=args.sampler))
     stream = torch.cuda.current_stream(dev)
@@ -416,7 +435,7 @@ def bench_ours(args):
     def launch():
         stats[8:].zero_()  # per-launch first/last warp exit words
         _lib.check(lib.fw_walk_device(handle, starts.data_ptr(), n, base_qid, ctypes.byref(a_s),
-                                      ctypes.byref(e_s), 0, seq.data_ptr(), lens.data_ptr(),
+                                      ctypes.byref(e_s), 0, seq_ptr, len_ptr,
                                       stats.data_ptr(), stream.cuda_stream))
 
     for _ in range(args.warmup):
@@ -440,7 +459,14 @@ def bench_ours(args):
         dist.barrier()
     launch_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     gather_ms = None
-    if world > 1 and not args.no_gather and args.scaling == "strong":
+    if gather == "direct":
+        # every rank's stores reached rank 0's buffer when its kernels
+        # finished (synchronized above, then the barrier): no gather phase
+        gather_ms = 0.0
+        if args.dump_gather and rank == 0:  # consumed by tests/test_gpu_parity.py
+            np.savez(args.dump_gather, seq=shared[0].view(n_total, L).cpu().numpy().view(np.uint32),
+                     lens=shared[1].cpu().numpy().view(np.uint32))
+    elif gather == "nccl":
         # rank 0 receives every other rank's segment (NCCL send/recv); the
         # time is the max over ranks of the device time around the exchange
         src_s, src_l = seq.to(cdev), lens.to(cdev)
@@ -569,8 +595,8 @@ def bench_ours(args):
             "dtype": "fp64+u64", "data": "synthetic",
             "config": workload_config(args, app, world),
             "run": {"replicate_s": None if world == 1 else round(t_rep, 3),
-                    "gather_ms": gather_ms,
-                    "gather_bytes": (n_total * L * 4 + n_total * 4) if gather_ms else None,
+                    "gather": gather, "gather_ms": gather_ms,
+                    "gather_bytes": (n_total * L * 4 + n_total * 4) if gather != "none" else None,
                     "per_rank_walk_ms": [round(x, 3) for x in per_rank_ms],
                     "backend": backend if world > 1 else None, "summation": summation,
                     "sampled_steps_per_gpu_step": sampled // args.steps,
@@ -581,6 +607,10 @@ def bench_ours(args):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if shared is not None:  # IPC views go before the exporting rank frees
+            del shared
+            torch.cuda.synchronize()
+            dist.barrier()
         dist.destroy_process_group()
 
 

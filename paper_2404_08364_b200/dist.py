@@ -8,7 +8,11 @@ There are two off-path exchanges:
   * replicate_csr: one source rank's CSR arrays are broadcast to all ranks
     (NCCL over NVLink for cuda tensors; gloo for CPU tensors in tests);
   * gather_paths: the per-rank (sequences, lengths) segments are sent
-    point-to-point to the destination rank, in qid order.
+    point-to-point to the destination rank, in qid order;
+  * share_buffers (the default in bench.py): no gather phase at all -- the
+    destination rank exports its result buffers by CUDA IPC and every rank's
+    walk kernel stores its path rows straight into them (NVLink peer stores,
+    fused with the walk; the rows are ~1 GB/s per GPU against 900 GB/s links).
 
 One process per GPU (torchrun); torch.distributed is plumbing only.
 """
@@ -70,3 +74,26 @@ def gather_paths(seq, lens, n_total, L, dst=0):
     for q in reqs:
         q.wait()
     return out_s.view(n_total, L), out_l
+
+
+def share_buffers(tensors, src=0):
+    """CUDA IPC: rank `src` exports its device tensors and every other rank
+    gets views of the same memory (opened with lazy peer access, so a kernel
+    on another GPU stores into it over NVLink; on one GPU it is plain shared
+    device memory).  Returns the list of tensors (src: its own).  The views
+    must be dropped before `src` frees the originals (call
+    release_shared() then barrier)."""
+    rank = dist.get_rank()
+    obj = [None]
+    if rank == src:
+        obj = [[(t.untyped_storage()._share_cuda_(), t.dtype, t.numel(), t.storage_offset())
+                for t in tensors]]
+    dist.broadcast_object_list(obj, src=src)
+    if rank == src:
+        return list(tensors)
+    views = []
+    for handle, dtype, numel, offset in obj[0]:
+        st = torch.UntypedStorage._new_shared_cuda(*handle)
+        dev = torch.device("cuda", handle[0])
+        views.append(torch.empty(0, dtype=dtype, device=dev).set_(st, offset, (numel,), (1,)))
+    return views

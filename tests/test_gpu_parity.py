@@ -181,11 +181,15 @@ def test_errors_raise_before_kernel(s16):
         fw.EngineConfig(k_big=1001).validate()
 
 
-def test_torchrun_two_ranks_strong_scaling_gather(tmp_path):
+@pytest.mark.parametrize("gather", ["direct", "nccl"])
+def test_torchrun_two_ranks_strong_scaling_gather(tmp_path, gather):
     """bench.py's multi-rank path end to end: 2 ranks (sharing this box's GPU,
     gloo for the control collectives), CSR generated on rank 0 and
     broadcast, qids partitioned (strong scaling), path segments gathered to
-    rank 0 -- the gathered paths must equal one oracle run over all qids."""
+    rank 0 -- either written straight into rank 0's buffer by every rank's
+    walk kernel (CUDA IPC, "direct") or sent point to point after the walk
+    ("nccl" mode; gloo here) -- the gathered paths must equal one oracle run
+    over all qids."""
     import json
     import os
     import subprocess
@@ -199,13 +203,15 @@ def test_torchrun_two_ranks_strong_scaling_gather(tmp_path):
            "--master-addr", "127.0.0.1", "--master-port", "29517",
            os.path.join(root, "bench.py"), "--gpus", "2", "--scale", "14", "--nq", str(n),
            "--steps", "1", "--warmup", "1",
-           "--dump-gather", str(out), "--no-cpu-baseline", "--no-e2e", "--length", "24"]
+           "--dump-gather", str(out), "--no-cpu-baseline", "--no-e2e", "--length", "24",
+           "--gather", gather]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert res.returncode == 0, res.stderr[-3000:]
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert line["config"]["queries_per_gpu"] == n // 2
-    assert line["run"]["gather_ms"] is not None and len(line["run"]["per_rank_walk_ms"]) == 2
+    assert line["run"]["gather"] == gather and line["run"]["gather_ms"] is not None
+    assert len(line["run"]["per_rank_walk_ms"]) == 2
     z = np.load(out)
     g = rmat.rmat_graph(14, labels=False)
     starts = np.arange(n, dtype=np.int64) % g.vertex_count

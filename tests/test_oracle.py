@@ -1,6 +1,8 @@
 """Pins the CPU oracle (oracle/walk_oracle.c) to the reference: golden walk
 vectors produced by running reswalk itself, and the RNG known answers."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -79,3 +81,26 @@ def test_oracle_thread_count_invariance(golden):
     b = oracle.walk(off, tgt, w, lab, starts, app="node2vec", length=24, threads=7)
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+def test_oracle_matches_reference_on_fuzz_cases():
+    """The oracle against the reference's own runs of 200 seeded random
+    configurations (tests/golden/fuzz.json): exotic lane widths and
+    thresholds, zero weights, self-loops, duplicates, every app."""
+    import json
+
+    import fuzz_cases
+    import oracle.ingest as ingest
+    with open(os.path.join(os.path.dirname(__file__), "golden", "fuzz.json")) as fh:
+        ref = {c["seed"]: c for c in json.load(fh)["cases"]}
+    for seed in range(fuzz_cases.N_CASES):
+        c = fuzz_cases.case(seed)
+        off, tgt, w, lab = ingest.build_csr(c["src"], c["dst"], c["w"], c["lab"], c["V"])
+        seq, ln, st = oracle.walk(off, tgt, w, lab, c["starts"], k_small=c["eng"]["k_small"],
+                                  k_big=c["eng"]["k_big"],
+                                  degree_threshold=c["eng"]["degree_threshold"],
+                                  sampler=c["eng"]["sampler"], seed=c["seed"], **c["app"])
+        want = ref[seed]
+        assert fuzz_cases.digest(ln.astype("<u4")) == want["len_sha256"], seed
+        assert fuzz_cases.digest(seq.astype("<u4")) == want["seq_sha256"], seed
+        assert st.tolist() == want["stats"], seed

@@ -1117,11 +1117,17 @@ __device__ uint32_t dprs_n2v_pow2(const WalkArgs &a, const StepCtx &s, uint32_t 
             uint32_t thr;
             if constexpr (!CERT) {
                 thr = accept_thr_raw(a.accept_wmax_s, (float)icarry);
-            } else if constexpr (F32) {
-                thr = accept_thr_f(fmaxf(fmaxf(wp[0], wp[1]), fmaxf(wp[2], wp[3])), (float)icarry);
             } else {
-                thr = accept_thr_f(__double2float_ru(fmax(fmax(wqv[0], wqv[1]), fmax(wqv[2], wqv[3]))),
-                                   (float)icarry);
+                // the quantized carry may overstate the exact one by 0.5 per
+                // element (weights rounded up): the prefilter needs a lower
+                // bound, carry - 0.5 * (elements before this tile <= x0)
+                // (fp32: its rounding is far inside the prefilter's 2^-12 margin)
+                const float clb = fmaxf(fmaf(-0.5f, (float)x0, (float)icarry), 0.0f);
+                if constexpr (F32)
+                    thr = accept_thr_f(fmaxf(fmaxf(wp[0], wp[1]), fmaxf(wp[2], wp[3])), clb);
+                else
+                    thr = accept_thr_f(
+                        __double2float_ru(fmax(fmax(wqv[0], wqv[1]), fmax(wqv[2], wqv[3]))), clb);
             }
             const uint32_t slo = __reduce_add_sync(FULL, li & 0xFFFFu);
             const uint32_t shi = __reduce_add_sync(FULL, li >> 16);

@@ -185,3 +185,25 @@ def test_every_golden_case_in_certified_mode(golden, name):
     np.testing.assert_array_equal(ln, want_len)
     np.testing.assert_array_equal(seq, want_seq)
     assert [getattr(st, f) for f in STAT_NAMES] == want_stats.tolist()
+
+
+@pytest.mark.parametrize("wbig,wlo,whi", [(5.0e8, 0.9, 1.1), (2.0e8, 0.28, 0.32),
+                                           (2.0e8, 0.26, 0.4), (1.0e9, 0.9, 1.1)])
+def test_quantized_sums_with_tiny_scaled_weights(wbig, wlo, whi):
+    """One huge edge weight puts every other scaled weight near 0.5-1 units of
+    the quantized integer sums, so the integer carry overstates the exact one
+    by up to 2x: the prefilter must still never reject an element the
+    reference accepts (its bound uses carry - 0.5 per element)."""
+    g = rmat.rmat_graph(12)
+    w = np.random.default_rng(9).uniform(wlo, whi, g.edge_count).astype(np.float32)
+    w[np.argmax(np.diff(g.offsets))] = np.float32(wbig)  # one edge somewhere
+    g = fw.Graph(g.vertex_count, g.edge_count, g.offsets, g.targets, w, g.labels)
+    starts = np.arange(g.vertex_count, dtype=np.int64)
+    app = dict(app="node2vec", length=30, a=2.0, b=0.5)
+    with _env(FW_FORCE_CERT="1"):
+        seq, ln, st = _run(g, starts, fw.AppConfig(**app), fw.EngineConfig(replay=True))
+    assert st.summation == "certified"
+    oseq, oln, ost = oracle.walk(g.offsets, g.targets, g.weights, g.labels, starts, **app)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq, oseq)
+    assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()

@@ -3,7 +3,7 @@ check and tests/golden/gen_fuzz.py (which ran the reference on them): small
 skewed edge lists (isolated vertices, self-loops, duplicates, optional
 symmetrisation), every app, random lengths / stop probabilities / schemas /
 (a, b), lane widths and degree thresholds, both samplers, uniform / integer /
-log-normal / zero-heavy weights, seeds up to 2^63."""
+log-normal / zero-heavy / one-huge-weight weights, seeds up to 2^63."""
 
 import numpy as np
 
@@ -20,7 +20,7 @@ def case(seed):
     if rs.random() < 0.5:  # symmetrise (the R-MAT workload's shape)
         src, dst = np.concatenate([src, dst]), np.concatenate([dst, src])
     src, dst = src.astype(np.uint32), dst.astype(np.uint32)
-    kind = rs.integers(0, 4)
+    kind = rs.integers(0, 5)
     E = len(src)
     if kind == 0:
         w = rs.uniform(1.0, 5.0, E)
@@ -28,8 +28,12 @@ def case(seed):
         w = rs.integers(0, 4, E).astype(np.float64)  # integers, zeros included
     elif kind == 2:
         w = rs.lognormal(0.0, 1.5, E)
-    else:
+    elif kind == 3:
         w = np.where(rs.random(E) < 0.2, 0.0, rs.random(E))
+    else:  # one huge weight: the others sit near the quantized sums' resolution
+        w = rs.uniform(0.2, 0.7, E)
+        if E:
+            w[int(rs.integers(0, E))] = float(rs.choice([1e6, 2e8, 1e9, 3e12]))
     lab = rs.integers(0, 5, E).astype(np.uint8)
     app_name = ["deepwalk", "ppr", "node2vec", "metapath"][seed % 4]
     app = dict(app=app_name, length=int(rs.integers(1, 40)), weighted=bool(rs.random() < 0.8))

@@ -93,6 +93,36 @@ def test_s22_node2vec_blocks(s22, block):
         assert st.large_tasks >= nq and st.edges_scanned > nq * host.max_degree()
 
 
+@pytest.mark.parametrize("block", ["interior", "hub"])
+def test_s22_node2vec_lognormal_certified_blocks(s22, block):
+    """The certified mode at the benchmark's scale: the s22 graph with
+    log-normal weights (bench.py --weights lognormal; sums round, so the walk
+    runs tree-order integer sums with certified accept tests), against the
+    oracle's sequential sums on the same qids."""
+    import torch
+    dg0, host0 = s22
+    E = host0.edge_count
+    w = np.random.default_rng(2).lognormal(0.0, 1.0, E).astype(np.float32)
+    wd = torch.empty(E + 4, dtype=torch.float32, device="cuda")[:E]
+    wd.copy_(torch.from_numpy(w))
+    from paper_2404_08364_b200.engine import DeviceGraph
+    dg = DeviceGraph(host0.vertex_count, E, dg0.offsets, dg0.targets, wd, None, device=0)
+    host = fw.Graph(host0.vertex_count, E, host0.offsets, host0.targets, w, None)
+    V, nq = host.vertex_count, 1024
+    base = 3_000_000 if block == "interior" else 777_777
+    starts = (np.full(nq, host.max_degree_vertex(), np.int64) if block == "hub"
+              else np.arange(base, base + nq, dtype=np.int64))
+    seq, ln, st = _gpu(dg, starts, N2V, base)
+    assert st.summation == "certified"
+    oseq, oln, ost = oracle.walk(host.offsets, host.targets, host.weights, None, starts,
+                                 app="node2vec", length=80, a=2.0, b=0.5, base_qid=base,
+                                 threads=THREADS)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(seq, oseq)
+    assert [getattr(st, f) for f in STAT_NAMES] == ost.tolist()
+    dg.close()
+
+
 def test_s22_node2vec_out_of_hub_chi_square(s22):
     """Second-order transitions out of the s22 hub: start at s0 (a neighbour
     of the hub with a sizable N(s0)); conditioned on the first hop being the

@@ -5,7 +5,6 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import case_kwargs
 import paper_2404_08364_b200 as fw
 from paper_2404_08364_b200 import rmat
 
